@@ -1,0 +1,177 @@
+"""Deterministic pre-simulation / event engine (oracle; test infrastructure).
+
+PAPER.md:530 — "once Inter-Dimension Schedules are determined, Themis simulates
+their execution to get an estimation of when each chunk operation will be
+available on each dimension ... enforces this intra-dimension ordering";
+:532 — the simulation is deterministic, so all NPUs produce the same order.
+PAPER.md:450-459 (§4.3) — intra-dimension policy: FIFO, or Smallest-Chunk-First.
+PAPER.md:281 — chunks are fed through the 2D-stage pipeline; a chunk's next
+stage starts after its previous stage.
+PAPER.md:464-471 — Latency(dimK) = A_K + N_K*B_K + idle_K.
+PAPER.md:292 — average BW utilisation = BW-weighted average of per-dim
+utilisation.  Table 3 (:551) — Ideal.
+
+Model (readings R9-R14):
+  * one server per dimension, one op at a time (R12); every chunk's first
+    stage is ready at t = 0;
+  * op duration = volume * B_K (+ A_K(phase) only if charge_latency, F5);
+  * at each time t all completions are processed first (the successor becomes
+    ready at t), then every idle dim starts its best ready op (R11);
+  * FIFO key (ready, chunk) (R10); SCF key (volume on that dim, ready, chunk)
+    (R9); 'scf_literal' key (bytes_before, chunk);
+  * idle_K = time dim K is idle before its last op completes, so
+    finish_K = busy_K + idle_K exactly and makespan = max_K finish_K;
+  * util = sum BW_K busy_K / (sum BW * makespan) (R14);
+  * Ideal = algorithmic bytes / sum BW (R13): 2S(P-1)/P for AR.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+from .collectives import AG, RS, bytes_sent, fixed_delay, size_after
+from .scheduler import AR, Schedule
+
+FIFO, SCF, SCF_LITERAL = "fifo", "scf", "scf_literal"
+
+
+@dataclass(frozen=True)
+class Op:
+    chunk: int
+    stage: int
+    dim: int
+    phase: str
+    bytes_before: Fraction
+    volume: Fraction          # n_K^i
+    duration: Fraction
+
+
+@dataclass
+class RunMetrics:
+    makespan: Fraction
+    busy: list
+    idle: list
+    finish: list
+    volume: list                                   # N_K
+    dim_order: list                                # per dim [(chunk, stage)]
+    start: dict = field(default_factory=dict)      # (chunk, stage) -> start
+    end: dict = field(default_factory=dict)        # (chunk, stage) -> end
+    util: Fraction = Fraction(0)
+    global_order: list = field(default_factory=list)  # [(chunk, stage)] by (start, dim)
+
+
+def chunk_ops(sched: Schedule, charge_latency: bool = False) -> list:
+    """Per chunk, its ops in stage order (size before each stage)."""
+    topo = sched.topo
+    out = []
+    for cs in sched.chunks:
+        b = sched.chunk_bytes if cs.rs else sched.chunk_bytes / topo.P
+        ops = []
+        for s, (d, ph) in enumerate(cs.stages()):
+            dim = topo.dims[d]
+            v = bytes_sent(ph, dim.size, b)
+            dur = v / dim.bw + (fixed_delay(dim, ph) if charge_latency else 0)
+            ops.append(Op(cs.chunk, s, d, ph, b, v, dur))
+            b = size_after(ph, dim.size, b)
+        out.append(ops)
+    return out
+
+
+def _key(policy: str, op: Op, ready):
+    if policy == FIFO:
+        return (ready, op.chunk)
+    if policy == SCF:
+        return (op.volume, ready, op.chunk)
+    if policy == SCF_LITERAL:
+        return (op.bytes_before, op.chunk)
+    raise ValueError(policy)
+
+
+def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
+             enforced=None) -> RunMetrics:
+    """Run the chunk pipelines.  With `enforced` (per-dim [(chunk, stage)]),
+    each dim must start its ops in exactly that order (the runtime contract,
+    PAPER.md:530); raises RuntimeError on deadlock."""
+    topo = sched.topo
+    D = topo.D
+    ops = chunk_ops(sched, charge_latency)
+    total = sum(len(o) for o in ops)
+    queue = [dict() for _ in range(D)]          # (chunk, stage) -> ready time
+    for c, o in enumerate(ops):
+        if o:
+            queue[o[0].dim][(c, 0)] = Fraction(0)
+    running = [None] * D                        # (chunk, stage, end)
+    pos = [0] * D
+    m = RunMetrics(Fraction(0), [Fraction(0)] * D, [Fraction(0)] * D, [Fraction(0)] * D,
+                   [Fraction(0)] * D, [[] for _ in range(D)])
+    t = Fraction(0)
+    done = 0
+    while done < total:
+        for k in range(D):                      # starts at time t
+            if running[k] is not None or not queue[k]:
+                continue
+            if enforced is not None:
+                if pos[k] >= len(enforced[k]):
+                    continue
+                nxt = tuple(enforced[k][pos[k]])
+                if nxt not in queue[k]:
+                    continue
+                pick = nxt
+                pos[k] += 1
+            else:
+                pick = min(queue[k], key=lambda cs: _key(policy, ops[cs[0]][cs[1]], queue[k][cs]))
+            del queue[k][pick]
+            op = ops[pick[0]][pick[1]]
+            running[k] = (pick[0], pick[1], t + op.duration)
+            m.start[pick] = t
+            m.dim_order[k].append(pick)
+            m.global_order.append(pick)
+            m.busy[k] += op.duration
+            m.volume[k] += op.volume
+        ends = [r[2] for r in running if r is not None]
+        if not ends:
+            raise RuntimeError("deadlock: no op running and unfinished ops remain")
+        t = min(ends)
+        for k in range(D):                      # completions at time t
+            r = running[k]
+            if r is None or r[2] != t:
+                continue
+            c, s, _ = r
+            running[k] = None
+            m.end[(c, s)] = t
+            m.finish[k] = t
+            done += 1
+            if s + 1 < len(ops[c]):
+                queue[ops[c][s + 1].dim][(c, s + 1)] = t
+    m.makespan = max(m.finish)
+    m.idle = [f - b for f, b in zip(m.finish, m.busy)]
+    tb = topo.total_bw
+    m.util = sum((d.bw * b for d, b in zip(topo.dims, m.busy)), Fraction(0)) / (tb * m.makespan)
+    return m
+
+
+def ideal_time(sched: Schedule) -> Fraction:
+    """Volume-based Ideal (reading R13): algorithmic bytes per NPU / sum BW."""
+    topo = sched.topo
+    f = Fraction(topo.P - 1, topo.P) * sched.total_bytes
+    if sched.coll == AR:
+        f *= 2
+    return f / topo.total_bw
+
+
+def activity_rate(m: RunMetrics, sched: Schedule, window) -> list:
+    """Fig 7: per dim, the fraction of each window during which
+    the dim has an op in service."""
+    window = Fraction(window)
+    nwin = max(1, -(-m.makespan // window))
+    out = []
+    for k in range(sched.topo.D):
+        iv = [(m.start[cs], m.end[cs]) for cs in m.dim_order[k]]
+        row = []
+        for w in range(int(nwin)):
+            a, b = w * window, min((w + 1) * window, m.makespan)
+            cov = sum((max(Fraction(0), min(b, e) - max(a, s)) for s, e in iv), Fraction(0))
+            row.append(cov / (b - a))
+        out.append(row)
+    return out

@@ -1,0 +1,171 @@
+"""Pins for the oracle's data All-Reduce over P simulated ranks."""
+
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import data as O, scheduler as S, engine as E, topology as T
+from synth import host_inputs
+
+LAYOUT = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "layout_2x2.json")))
+
+
+def _sched(topo, coll, N, esize, C, orders):
+    chunks = []
+    for c, rs in enumerate(orders):
+        if coll == S.AR:
+            chunks.append(S.ChunkSchedule(c, tuple(rs), tuple(reversed(rs))))
+        elif coll == "RS":
+            chunks.append(S.ChunkSchedule(c, tuple(rs), ()))
+        else:
+            chunks.append(S.ChunkSchedule(c, (), tuple(rs)))
+    from fractions import Fraction
+    return S.Schedule(topo, coll, Fraction(N * esize), C, chunks, [], 0)
+
+
+def test_layout_hand_example():
+    t = T.Topology.make(LAYOUT["sizes"], (1, 1))
+    x = [np.array(v, dtype=np.int32) for v in LAYOUT["inputs"]]
+    # after RS on dim1 only
+    s = _sched(t, "RS", 4, 4, 1, [(0, 1)])
+    b = O.run_schedule(x, s, "i32", order=[(0, 0)])
+    for blk, v in LAYOUT["after_rs_dim1_first"]["rank0"].items():
+        assert b[0][int(blk)] == v
+    s = _sched(t, "RS", 4, 4, 1, [(1, 0)])
+    b = O.run_schedule(x, s, "i32", order=[(0, 0)])
+    for blk, v in LAYOUT["after_rs_dim2_first"]["rank0"].items():
+        assert b[0][int(blk)] == v
+    for order in [(0, 1), (1, 0)]:
+        rs = O.run_schedule(x, _sched(t, "RS", 4, 4, 1, [order]), "i32")
+        assert [int(rs[r][r]) for r in range(4)] == LAYOUT["rs_result_block_r"]["value"]
+        ar = O.run_schedule(x, _sched(t, S.AR, 4, 4, 1, [order]), "i32")
+        for r in range(4):
+            assert ar[r].tolist() == LAYOUT["ar_result"]
+
+
+def _random_case(rng, maxD=3):
+    D = rng.randint(1, maxD)
+    sizes = [rng.choice([2, 3, 4]) for _ in range(D)]
+    t = T.Topology.make(sizes, [rng.randint(1, 4) for _ in range(D)])
+    C = rng.randint(1, 4)
+    N = t.P * C * rng.randint(1, 3)
+    return t, C, N
+
+
+def test_int32_allreduce_exact_any_order():
+    """Integer sums are exact (mod 2^32), so every RS/AG order must reproduce
+    the plain definition sum_r x_r bit for bit on every rank (PAPER.md:221,
+    Observation 1 :420: stage order does not affect correctness)."""
+    rng = random.Random(1)
+    for _ in range(40):
+        t, C, N = _random_case(rng)
+        x = host_inputs(t.P, N, "i32", seed=rng.randint(0, 10 ** 6))
+        want = O.allreduce_definition(x, "i32")
+        perms = list(itertools.permutations(range(t.D)))
+        orders = [rng.choice(perms) for _ in range(C)]
+        out = O.run_schedule(x, _sched(t, S.AR, N, 4, C, orders), "i32")
+        for r in range(t.P):
+            assert np.array_equal(out[r], want)
+
+
+def test_int32_wraps():
+    t = T.Topology.make((2, 2), (1, 1))
+    x = [np.full(8, 2 ** 31 - 1, dtype=np.int32) for _ in range(4)]
+    out = O.run_schedule(x, _sched(t, S.AR, 8, 4, 2, [(0, 1), (1, 0)]), "i32")
+    assert out[0][0] == np.int32(-4)            # 4*(2^31-1) mod 2^32
+    assert np.array_equal(out[3], O.allreduce_definition(x, "i32"))
+
+
+def test_rs_then_ag_and_definitions():
+    rng = random.Random(2)
+    for _ in range(20):
+        t, C, N = _random_case(rng)
+        x = host_inputs(t.P, N, "i32", seed=rng.randint(0, 10 ** 6))
+        perms = list(itertools.permutations(range(t.D)))
+        rs_orders = [rng.choice(perms) for _ in range(C)]
+        ag_orders = [rng.choice(perms) for _ in range(C)]
+        rs = O.run_schedule(x, _sched(t, "RS", N, 4, C, rs_orders), "i32")
+        want = O.reduce_scatter_definition(x, "i32", t.P)
+        blk = N // t.P
+        for r in range(t.P):
+            assert np.array_equal(rs[r][r * blk:(r + 1) * blk], want[r])
+        ag = O.run_schedule(rs, _sched(t, "AG", N, 4, C, ag_orders), "i32")
+        full = O.allreduce_definition(x, "i32")
+        for r in range(t.P):
+            assert np.array_equal(ag[r], full)
+        # AG alone: concatenation of every rank's own block
+        ag2 = O.run_schedule(x, _sched(t, "AG", N, 4, C, ag_orders), "i32")
+        cat = O.all_gather_definition(x, t.P)
+        for r in range(t.P):
+            assert np.array_equal(ag2[r], cat)
+
+
+def test_float_error_bounds():
+    """fp32: |y - sum| <= (P-1) 2^-24 sum|x| (first-order summation bound);
+    bf16: one RNE rounding per RS stage -> <= D 2^-8 sum|x| (F10)."""
+    rng = random.Random(4)
+    for dtype, bound in (("f32", lambda t: (t.P - 1) * 2.0 ** -24), ("bf16", lambda t: t.D * 2.0 ** -8),
+                         ("f16", lambda t: t.D * 2.0 ** -11 + (t.P - 1) * 2.0 ** -24)):
+        for _ in range(8):
+            t, C, N = _random_case(rng)
+            x = host_inputs(t.P, N * 16, dtype, seed=rng.randint(0, 10 ** 6))
+            s = S.schedule_collective(t, S.AR, N * 16 * 2, C, S.THEMIS)
+            out = O.run_schedule(x, s, dtype)
+            ref = O.allreduce_definition(x, dtype)
+            scale = O.abs_sum(x, dtype)
+            for r in range(t.P):
+                err = np.abs(O.to_f64(out[r], dtype) - ref)
+                assert np.all(err <= bound(t) * scale + 1e-30)
+            # all ranks bitwise identical
+            for r in range(1, t.P):
+                assert np.array_equal(out[r].view(np.uint8), out[0].view(np.uint8))
+
+
+def test_d1_is_textbook_direct_allreduce():
+    """D = 1 reduces to the flat direct RS+AG (Table 1 'Direct'): every rank
+    gets x_0 + x_1 + ... + x_{P-1} summed left to right in fp32."""
+    t = T.Topology.make((4,), (1,))
+    x = host_inputs(4, 64, "f32")
+    out = O.run_schedule(x, _sched(t, S.AR, 64, 4, 2, [(0,), (0,)]), "f32")
+    want = ((x[0] + x[1]) + x[2]) + x[3]
+    for r in range(4):
+        assert np.array_equal(out[r], want)
+
+
+def test_bf16_rne_matches_torch():
+    """The oracle's fp32 -> bf16 rounding equals torch's conversion
+    (round-to-nearest-even), including ties, denormals, inf and NaN."""
+    g = torch.Generator().manual_seed(0)
+    v = torch.randn(100000, generator=g) * torch.exp(torch.randn(100000, generator=g) * 20)
+    ties = torch.tensor([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 2 ** -130, float("inf"),
+                         -float("inf"), 3.3895313892515355e38, 1e-45])
+    v = torch.cat([v, ties])
+    mine = O.f32_to_bf16(v.numpy())
+    ref = v.to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(mine, ref)
+    nan = O.f32_to_bf16(np.array([np.nan], dtype=np.float32))
+    assert np.isnan(O.bf16_to_f32(nan))[0]
+
+
+def test_order_from_simulation_equals_chunk_order():
+    t = T.Topology.make((2, 2, 2), (1, 1, 1))
+    C, N = 8, 8 * 8 * 4
+    x = host_inputs(8, N, "f32")
+    s = S.schedule_collective(t, S.AR, N * 4, C, S.THEMIS)
+    m = E.simulate(s, E.SCF)
+    a = O.run_schedule(x, s, "f32", order=m.global_order)
+    b = O.run_schedule(x, s, "f32")
+    for r in range(8):
+        assert np.array_equal(a[r], b[r])
+
+
+def test_rejects_bad_sizes():
+    t = T.Topology.make((2, 2), (1, 1))
+    x = [np.zeros(6, np.int32)] * 4
+    with pytest.raises(ValueError):
+        O.run_schedule(x, _sched(t, S.AR, 6, 4, 1, [(0, 1)]), "i32")
