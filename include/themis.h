@@ -1,0 +1,224 @@
+/*
+ * themis.h — C ABI of libthemis: the B200-native hot path of Themis
+ * (arXiv 2110.04478): a chunked hierarchical All-Reduce (and its
+ * Reduce-Scatter / All-Gather halves) over a logical P_1 x ... x P_D topology,
+ * each chunk traversing the dimensions in the order Themis's greedy policy
+ * (Algorithm 1) picks, executed by hand-written sm_100a kernels that pull peer
+ * data over NVLink / NVSwitch.
+ *
+ * Citations are to /root/reference/PAPER.md lines; "R<n>" are the readings
+ * listed in DESIGN.md where the paper is silent or ambiguous.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns themis_status_t; THEMIS_OK == 0.  No C++ exception
+ *     crosses the ABI.  themis_last_error() returns a thread-local message for
+ *     the last failing call on the calling thread.
+ *   - Pointers marked [host] are host memory, [device] are device memory (or
+ *     UVA pointers to a peer GPU's memory), [out] are written by the call.
+ *   - Collectives are enqueue-only and asynchronous on the given CUDA stream.
+ *     Device-side failures (watchdog timeout) are latched in the comm and
+ *     reported by the next collective call or themis_comm_status().
+ *   - Objects are owned by the caller: every *_create / plan has a matching
+ *     *_free.  The library never frees memory it did not allocate.
+ *
+ * Units: bandwidth in MB/s (10^6 bytes/s, integer), latency in ns, sizes in
+ * bytes.  Planner arithmetic is exact (integers, 128-bit intermediates); time
+ * is reported in integer units of 1/time_scale ns and per-dimension volumes in
+ * units of 1/byte_scale bytes (themis_plan_info_t), so schedules and
+ * predicted times are bit-exact against the oracle's rational arithmetic.
+ */
+#ifndef THEMIS_H_
+#define THEMIS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define THEMIS_MAX_DIMS 8      /* D <= 8 (the paper uses D <= 4, Table 2) */
+#define THEMIS_MAX_CHUNKS 1024 /* CPC <= 1024 (paper: 4..512) */
+#define THEMIS_MAX_GPUS 8      /* GPUs of one NVSwitch box */
+#define THEMIS_IPC_HANDLE_BYTES 64
+
+typedef enum {
+  THEMIS_OK = 0,
+  THEMIS_ERR_INVALID_ARG = 1,     /* malformed topology / request / argument */
+  THEMIS_ERR_ALIGNMENT = 2,       /* count not a multiple of P*C*vec, or misaligned buf */
+  THEMIS_ERR_UNSUPPORTED_DTYPE = 3,
+  THEMIS_ERR_OVERFLOW = 4,        /* exact planner arithmetic would overflow */
+  THEMIS_ERR_NOT_REGISTERED = 5,  /* buf outside the comm's registered heap */
+  THEMIS_ERR_PLAN_MISMATCH = 6,   /* plan not bound / bound to another comm / wrong coll */
+  THEMIS_ERR_CUDA = 7,            /* a CUDA runtime call failed (message has details) */
+  THEMIS_ERR_TIMEOUT = 8          /* device watchdog fired (peer never signalled) */
+} themis_status_t;
+
+typedef enum { THEMIS_F32 = 0, THEMIS_BF16 = 1, THEMIS_F16 = 2, THEMIS_I32 = 3 } themis_dtype_t;
+typedef enum { THEMIS_ALLREDUCE = 0, THEMIS_REDUCE_SCATTER = 1, THEMIS_ALL_GATHER = 2 } themis_coll_t;
+/* Table 3: Baseline = fixed dim1->dimD order;
+ * Themis = Algorithm 1. */
+typedef enum { THEMIS_POLICY_BASELINE = 0, THEMIS_POLICY_THEMIS = 1 } themis_policy_t;
+/* Intra-dimension order: SCF keyed on the op's transfer volume
+ * (R9), FIFO (R10), or SCF keyed on bytes-before (SPEC.md:330 literal). */
+typedef enum { THEMIS_INTRA_SCF = 0, THEMIS_INTRA_FIFO = 1, THEMIS_INTRA_SCF_LITERAL = 2 } themis_intra_t;
+/* Table 1: per-dimension topology -> basic algorithm. */
+typedef enum { THEMIS_DIM_RING = 0, THEMIS_DIM_DIRECT = 1, THEMIS_DIM_SWITCH = 2 } themis_dim_kind_t;
+
+/* Logical topology P_1 x ... x P_D.  Rank r has coordinates
+ * c_k = floor(r / prod_{i<k} P_i) mod P_k (dim1 fastest, R15).
+ * bw[k]: aggregate uni-directional per-NPU bandwidth of dim k in MB/s
+ * (PAPER.md:505, :136); with zero latencies only the ratios matter.
+ * Validation: 1 <= ndims <= 8, size >= 2, bw > 0,
+ * SWITCH => size is a power of two. */
+typedef struct {
+  int32_t ndims;
+  int32_t size[THEMIS_MAX_DIMS];
+  uint32_t bw_mbps[THEMIS_MAX_DIMS];
+  uint32_t step_latency_ns[THEMIS_MAX_DIMS];
+  int32_t kind[THEMIS_MAX_DIMS]; /* themis_dim_kind_t */
+} themis_topology_t;
+
+/* One collective to plan (Algorithm 1 inputs CT, CS, CPC). */
+typedef struct {
+  int32_t coll;            /* themis_coll_t (CT) */
+  int32_t policy;          /* themis_policy_t */
+  int32_t intra;           /* themis_intra_t */
+  int32_t n_chunks;        /* CPC, 1..THEMIS_MAX_CHUNKS (paper default 64) */
+  uint64_t bytes;          /* CS: bytes of the full buffer on each rank (> 0) */
+  int32_t threshold_div;   /* Threshold = time of an RS/AG of chunk/threshold_div on
+                              the min-load dim (paper uses 16) */
+  int32_t charge_latency;  /* 0 (default, F5): the pre-simulation charges A_K only via
+                              the tracker seed; 1: also per op */
+} themis_plan_req_t;
+
+/* Summary of a plan.  Times in units of 1/time_scale ns, volumes in units of
+ * 1/byte_scale bytes (exact; see the header comment). */
+typedef struct {
+  int32_t ndims, n_chunks, n_ranks;
+  int32_t n_stages;        /* stages per chunk: 2D for AR, D for RS / AG */
+  int32_t n_greedy;        /* chunks whose order came from the sort (not the threshold fallback) */
+  int32_t coll, policy, intra;
+  uint64_t time_scale;     /* integer time units per ns */
+  uint64_t byte_scale;     /* integer volume units per byte (= P * C) */
+  uint64_t makespan;       /* predicted makespan of the pre-simulation */
+  uint64_t busy[THEMIS_MAX_DIMS];       /* N_K*B_K (+A_K if charged) */
+  uint64_t idle[THEMIS_MAX_DIMS];       /* idle_K: idle before dim K's last op ends */
+  uint64_t dim_volume[THEMIS_MAX_DIMS]; /* N_K = sum_i n_K^i, x byte_scale */
+  uint64_t final_load[THEMIS_MAX_DIMS]; /* Dim Load Tracker after the last chunk */
+  uint64_t hash;           /* FNV-1a of inputs + schedule + per-dim order; equal on all ranks */
+} themis_plan_info_t;
+
+typedef struct themis_plan themis_plan_t;
+typedef struct themis_comm themis_comm_t;
+
+/* ---------------------------------------------------------------- planner
+ * themis_plan: host-only, pure, thread-safe.  Runs the Splitter, the Dim Load
+ * Tracker seeded with A_K, Algorithm 1 with the Threshold
+ * or the baseline order, then the deterministic
+ * pre-simulation that fixes every dimension's op order.
+ * Errors: INVALID_ARG (validation), OVERFLOW.  *out is owned by the caller
+ * (themis_plan_free). */
+themis_status_t themis_plan(const themis_topology_t* topo /*[host]*/, const themis_plan_req_t* req /*[host]*/,
+                            themis_plan_t** out /*[out]*/);
+themis_status_t themis_plan_info(const themis_plan_t* plan, themis_plan_info_t* info /*[host, out]*/);
+/* Per-chunk dim orders, 0-based dims, row-major [C][D]; ag_order for AR is
+ * reverse(rs_order) (Algorithm 1 line 8).  RS plans leave ag_order rows 0xFF,
+ * AG plans leave rs_order rows 0xFF.  Either pointer may be NULL. */
+themis_status_t themis_plan_orders(const themis_plan_t* plan, uint8_t* rs_order /*[host,out] C*D*/,
+                                   uint8_t* ag_order /*[host,out] C*D*/);
+/* Per-dimension enforced op order: dim_ops[k*(C*n_stages) + i] = (chunk << 8) | stage,
+ * n_dim_ops[k] entries valid per dim (row stride C*n_stages).  Every rank
+ * executes exactly this order on each dimension. */
+themis_status_t themis_plan_dim_ops(const themis_plan_t* plan, uint32_t* dim_ops /*[host,out] D*C*n_stages*/,
+                                    int32_t* n_dim_ops /*[host,out] D*/);
+/* Pre-simulated start / end time of every op, [C][n_stages], time units. */
+themis_status_t themis_plan_times(const themis_plan_t* plan, uint64_t* start /*[host,out]*/,
+                                  uint64_t* end /*[host,out]*/);
+void themis_plan_free(themis_plan_t* plan);
+
+/* ---------------------------------------------------------------- memory
+ * A comm spans W GPUs (one process each) hosting P = prod P_k logical ranks,
+ * V = P / W consecutive ranks per GPU (V > 1 emulates several ranks on one
+ * GPU: W = 1 runs the whole topology inside one GPU's HBM).  Each GPU owns
+ * one "heap": [V signal pads of themis_signal_bytes(P) each][V data regions
+ * of vrank_stride bytes].  Peers' heaps are mapped with CUDA IPC.
+ * themis_heap_layout: signal bytes per pad and total heap bytes for
+ * V ranks with data_bytes per rank (data_bytes rounded up to 4 KiB). */
+themis_status_t themis_heap_layout(int32_t n_ranks, int32_t n_gpus, uint64_t data_bytes,
+                                   uint64_t* signal_bytes /*[out]*/, uint64_t* vrank_stride /*[out]*/,
+                                   uint64_t* heap_bytes /*[out]*/);
+/* cudaMalloc on the current device, signal pads zeroed.  Caller frees. */
+themis_status_t themis_heap_alloc(uint64_t heap_bytes, void** heap /*[out, device]*/);
+themis_status_t themis_heap_free(void* heap /*[device]*/);
+/* CUDA IPC handle of a heap (64 bytes) to send to the other processes. */
+themis_status_t themis_heap_export(void* heap /*[device]*/, uint8_t* handle /*[host,out] 64 B*/);
+/* Map a peer's heap into this process; returns its UVA base pointer. */
+themis_status_t themis_heap_import(const uint8_t* handle /*[host] 64 B*/, void** peer_heap /*[out]*/);
+themis_status_t themis_heap_close(void* peer_heap /*[device]*/);
+
+/* ---------------------------------------------------------------- comm
+ * gpu_rank / n_gpus: this process's index among the W GPUs.  heaps[g]: UVA
+ * base of GPU g's heap as mapped in this process (own heap at heaps[gpu_rank]).
+ * Allocates small device-local state (op counters, error word, trace).
+ * Errors: INVALID_ARG, CUDA. */
+themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, const themis_topology_t* topo /*[host]*/,
+                                   void* const* heaps /*[host] n_gpus UVA pointers*/, uint64_t heap_bytes,
+                                   uint64_t vrank_stride, themis_comm_t** out /*[out]*/);
+void themis_comm_free(themis_comm_t* comm);
+/* Latched asynchronous device errors (THEMIS_ERR_TIMEOUT) or THEMIS_OK.
+ * Non-blocking: reads a host-mapped error word the kernel writes. */
+themis_status_t themis_comm_status(themis_comm_t* comm);
+/* Copy engine of the kernel: 1 (default) = TMA bulk copies (cp.async.bulk)
+ * into a shared-memory ring + warp-specialised reduction; 0 = per-thread
+ * 16-byte LDG/STG.  Env THEMIS_COPY_ENGINE=ldg|tma sets the default. */
+themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
+/* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */
+themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
+/* Trace: when enabled, each dim group records %globaltimer start/end of every
+ * op it runs (PAPER.md:640/:658 activity).  Fetch after the stream is synced:
+ * out[(chunk*n_stages + stage)*2 + {0,1}] in ns, n = C*n_stages*2 entries. */
+themis_status_t themis_comm_enable_trace(themis_comm_t* comm, int32_t enable);
+themis_status_t themis_trace_fetch(themis_comm_t* comm, uint64_t* out /*[host,out]*/, size_t n);
+
+/* Attach a plan to a comm with per-dimension CTA counts.  ctas_per_dim[k] =
+ * CTAs (SMs) of dimension k's group; NULL = proportional to bw_mbps over all
+ * SMs.  Capping CTAs per dim emulates heterogeneous per-dimension bandwidth
+ * on the uniform NVSwitch fabric.  Uploads the per-dim op lists (the plan is
+ * immutable afterwards).  Errors: INVALID_ARG (topology differs from the
+ * comm's, too many CTAs for co-residency), CUDA. */
+themis_status_t themis_plan_bind(themis_plan_t* plan, themis_comm_t* comm, const int32_t* ctas_per_dim /*[host] D or NULL*/);
+/* CTAs per dimension group a bound plan launches with ([host, out] D entries).
+ * Errors: PLAN_MISMATCH if the plan is not bound. */
+themis_status_t themis_plan_bound_ctas(const themis_plan_t* plan, int32_t* ctas_per_dim /*[host,out]*/);
+
+/* ---------------------------------------------------------------- collectives
+ * buf: [device] local rank 0's data region inside this GPU's heap (local rank
+ * v's data is at buf + v*vrank_stride), the same offset on every GPU.
+ * count: elements of the FULL buffer on each rank (all three calls).
+ *   AR: every rank ends with sum_r x_r.
+ *   RS: rank r ends with block r of the sum at buf + r*count/P (in place).
+ *   AG: rank r's input block r is at buf + r*count/P; output is the full buffer.
+ * Requirements: count * elem_size == plan bytes; count % (P * C * (16/elem_size)) == 0
+ * (ALIGNMENT); the plan's coll matches the call (PLAN_MISMATCH); all ranks
+ * call the same collectives, with identical plans, in the same order.
+ * Float sums: fp32 accumulate in coordinate order within each stage, one
+ * round-to-nearest-even per RS stage for bf16/f16 (R18); int32 wraps (R19). */
+themis_status_t themis_allreduce(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
+themis_status_t themis_reduce_scatter(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
+themis_status_t themis_all_gather(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
+/* End-to-end All-Reduce with HOST buffers: copies host_in (V local ranks,
+ * contiguous, count elements each; pinned memory recommended) into the heap,
+ * runs themis_allreduce, copies the result to host_out; all on `stream`. */
+themis_status_t themis_allreduce_host(const void* host_in /*[host]*/, void* host_out /*[host,out]*/, void* buf,
+                                      uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
+
+/* Number of kernel launches the last collective call made (1 per call). */
+int32_t themis_launches_per_call(void);
+const char* themis_last_error(void);
+const char* themis_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* THEMIS_H_ */

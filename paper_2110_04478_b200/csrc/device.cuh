@@ -1,0 +1,243 @@
+// Device-side building blocks of the Themis executor (sm_100a).
+//
+// Memory-ordering protocol:
+//   producer CTA: data stores -> bar.sync -> fence.sc.sys -> op counter atomic;
+//   the CTA that completes an op publishes epoch-tagged flags with
+//   st.release.sys into the signal pads of the ranks that consume it;
+//   consumers spin with ld.acquire.sys on their own (local) pad, then bar.sync,
+//   then read peer data with L1-bypassing ld.global.cg.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace themis {
+namespace dev {
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 16-byte vector moves.  .cg: cache in L2 only (no stale L1 lines for data
+// other CTAs / GPUs wrote during this launch).
+__device__ __forceinline__ uint4 ld_cg(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---- elementwise accumulate of one 16-byte vector, per dtype -------------
+// Accumulator layout: 4 x f32 (f32), 8 x f32 (bf16/f16, one vector of 8
+// elements), 4 x i32 (i32).  The sum is taken in coordinate order (R18).
+struct F32Tag {
+  static constexpr int kAcc = 4;
+  __device__ static void load(float* a, const uint4& v) {
+    a[0] = __uint_as_float(v.x); a[1] = __uint_as_float(v.y);
+    a[2] = __uint_as_float(v.z); a[3] = __uint_as_float(v.w);
+  }
+  __device__ static void add(float* a, const uint4& v) {
+    a[0] = __fadd_rn(a[0], __uint_as_float(v.x)); a[1] = __fadd_rn(a[1], __uint_as_float(v.y));
+    a[2] = __fadd_rn(a[2], __uint_as_float(v.z)); a[3] = __fadd_rn(a[3], __uint_as_float(v.w));
+  }
+  __device__ static uint4 store(const float* a) {
+    return make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]), __float_as_uint(a[3]));
+  }
+};
+
+struct BF16Tag {
+  static constexpr int kAcc = 8;
+  __device__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
+  __device__ static float hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+  __device__ static void load(float* a, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { a[2 * i] = lo(w[i]); a[2 * i + 1] = hi(w[i]); }
+  }
+  __device__ static void add(float* a, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[2 * i] = __fadd_rn(a[2 * i], lo(w[i]));
+      a[2 * i + 1] = __fadd_rn(a[2 * i + 1], hi(w[i]));
+    }
+  }
+  __device__ static uint32_t pack(float x, float y) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(x, y);  // round to nearest even
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __device__ static uint4 store(const float* a) {
+    return make_uint4(pack(a[0], a[1]), pack(a[2], a[3]), pack(a[4], a[5]), pack(a[6], a[7]));
+  }
+};
+
+struct F16Tag {
+  static constexpr int kAcc = 8;
+  __device__ static void load(float* a, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      a[2 * i] = f.x; a[2 * i + 1] = f.y;
+    }
+  }
+  __device__ static void add(float* a, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      a[2 * i] = __fadd_rn(a[2 * i], f.x); a[2 * i + 1] = __fadd_rn(a[2 * i + 1], f.y);
+    }
+  }
+  __device__ static uint4 store(const float* a) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = __floats2half2_rn(a[2 * i], a[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+struct I32Tag {  // wraps mod 2^32 (R19); float slots hold raw bits
+  static constexpr int kAcc = 4;
+  __device__ static void load(float* a, const uint4& v) {
+    a[0] = __uint_as_float(v.x); a[1] = __uint_as_float(v.y);
+    a[2] = __uint_as_float(v.z); a[3] = __uint_as_float(v.w);
+  }
+  __device__ static void add(float* a, const uint4& v) {
+    a[0] = __uint_as_float(__float_as_uint(a[0]) + v.x); a[1] = __uint_as_float(__float_as_uint(a[1]) + v.y);
+    a[2] = __uint_as_float(__float_as_uint(a[2]) + v.z); a[3] = __uint_as_float(__float_as_uint(a[3]) + v.w);
+  }
+  __device__ static uint4 store(const float* a) {
+    return make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]), __float_as_uint(a[3]));
+  }
+};
+
+// ---- the hot loops ---------------------------------------------------------
+// RS piece: dst[u] = src[0][u] + src[1][u] + ... + src[n-1][u] for 16-byte
+// vectors u in [a, e), all NSRC loads of UNROLL vectors issued before any add
+// so that NSRC*UNROLL 16-byte requests are in flight per thread.
+template <class Tag, int NSRC, int UNROLL, class Src>
+__device__ __forceinline__ void reduce_range(uint4* __restrict__ dst, const Src& src, uint64_t a, uint64_t e) {
+  const uint64_t step = (uint64_t)blockDim.x * UNROLL;
+  const uint4* s[NSRC];
+#pragma unroll
+  for (int j = 0; j < NSRC; ++j) s[j] = src(j);
+#pragma unroll 1
+  for (uint64_t u = a + threadIdx.x; u < e; u += step) {
+    uint4 x[NSRC][UNROLL];
+#pragma unroll
+    for (int r = 0; r < UNROLL; ++r) {
+      const uint64_t uu = u + (uint64_t)r * blockDim.x;
+      if (uu < e) {
+#pragma unroll
+        for (int j = 0; j < NSRC; ++j) x[j][r] = ld_cg(s[j] + uu);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < UNROLL; ++r) {
+      const uint64_t uu = u + (uint64_t)r * blockDim.x;
+      if (uu < e) {
+        float acc[Tag::kAcc];
+        Tag::load(acc, x[0][r]);
+#pragma unroll
+        for (int j = 1; j < NSRC; ++j) Tag::add(acc, x[j][r]);
+        st_v4(dst + uu, Tag::store(acc));
+      }
+    }
+  }
+}
+
+// Generic source count (P_k > 8): one source at a time, still in order.
+template <class Tag, class Src>
+__device__ __forceinline__ void reduce_range_generic(uint4* __restrict__ dst, const Src& src, int n, uint64_t a,
+                                                     uint64_t e) {
+#pragma unroll 1
+  for (uint64_t u = a + threadIdx.x; u < e; u += blockDim.x) {
+    float acc[Tag::kAcc];
+    Tag::load(acc, ld_cg(src(0) + u));
+    for (int j = 1; j < n; ++j) Tag::add(acc, ld_cg(src(j) + u));
+    st_v4(dst + u, Tag::store(acc));
+  }
+}
+
+// AG piece: bitwise copy of 16-byte vectors [a, e).
+template <int UNROLL>
+__device__ __forceinline__ void copy_range(uint4* __restrict__ dst, const uint4* __restrict__ src, uint64_t a,
+                                           uint64_t e) {
+  const uint64_t step = (uint64_t)blockDim.x * UNROLL;
+#pragma unroll 1
+  for (uint64_t u = a + threadIdx.x; u < e; u += step) {
+    uint4 x[UNROLL];
+#pragma unroll
+    for (int r = 0; r < UNROLL; ++r) {
+      const uint64_t uu = u + (uint64_t)r * blockDim.x;
+      if (uu < e) x[r] = ld_cg(src + uu);
+    }
+#pragma unroll
+    for (int r = 0; r < UNROLL; ++r) {
+      const uint64_t uu = u + (uint64_t)r * blockDim.x;
+      if (uu < e) st_v4(dst + uu, x[r]);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace themis
+
+namespace themis {
+namespace dev {
+// ---- mbarrier + bulk async copy (TMA engine, no tensor map needed) --------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global (local HBM or a peer GPU over NVLink) -> shared, completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+}  // namespace dev
+}  // namespace themis

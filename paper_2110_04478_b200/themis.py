@@ -1,0 +1,308 @@
+"""Thin Python binding of libthemis (include/themis.h).
+
+Argument marshalling only.  The names mirror the C ABI
+(``themis_plan``, ``themis_allreduce``, ``themis_reduce_scatter``,
+``themis_all_gather`` ...); ``Plan`` / ``Comm`` are small RAII wrappers around
+the opaque handles.  PyTorch is used for device selection, streams and — for
+multi-process comms — the process group that exchanges CUDA IPC handles.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import (IPC_HANDLE_BYTES, MAX_DIMS, MAX_GPUS, PlanInfo_t, PlanReq_t, ThemisError, Topology_t, check,
+                   lib)
+
+RING, DIRECT, SWITCH = 0, 1, 2                 # Table 1
+ALLREDUCE, REDUCE_SCATTER, ALL_GATHER = 0, 1, 2
+BASELINE, THEMIS = 0, 1                        # Table 3
+SCF, FIFO, SCF_LITERAL = 0, 1, 2               # §4.3
+DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "i32": 3}
+ELEM_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4}
+COLL_NAMES = {"AR": ALLREDUCE, "RS": REDUCE_SCATTER, "AG": ALL_GATHER}
+
+
+@dataclass(frozen=True)
+class Topology:
+    """P_1 x ... x P_D; bw in MB/s per dimension."""
+    sizes: tuple
+    bw_mbps: tuple
+    kinds: tuple = field(default=None)
+    latency_ns: tuple = field(default=None)
+
+    @property
+    def D(self) -> int:
+        return len(self.sizes)
+
+    @property
+    def P(self) -> int:
+        return int(np.prod(self.sizes))
+
+    def to_c(self) -> Topology_t:
+        t = Topology_t()
+        t.ndims = self.D
+        kinds = self.kinds or (DIRECT,) * self.D
+        lat = self.latency_ns or (0,) * self.D
+        for k in range(self.D):
+            t.size[k] = int(self.sizes[k])
+            t.bw_mbps[k] = int(self.bw_mbps[k])
+            t.step_latency_ns[k] = int(lat[k])
+            t.kind[k] = int(kinds[k])
+        return t
+
+
+def themis_plan(topo: Topology, coll: int, nbytes: int, n_chunks: int, policy: int = THEMIS, intra: int = SCF,
+                threshold_div: int = 16, charge_latency: bool = False) -> C.c_void_p:
+    req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency))
+    out = C.c_void_p()
+    tc = topo.to_c()
+    check(lib().themis_plan(C.byref(tc), C.byref(req), C.byref(out)))
+    return out
+
+
+class Plan:
+    """A Themis (or baseline) plan: per-chunk dim orders + per-dim op order."""
+
+    def __init__(self, topo: Topology, coll: int = ALLREDUCE, nbytes: int = 0, n_chunks: int = 64,
+                 policy: int = THEMIS, intra: int = SCF, threshold_div: int = 16, charge_latency: bool = False):
+        self.topo = topo
+        self.coll = coll
+        self.nbytes = int(nbytes)
+        self.n_chunks = n_chunks
+        self.policy = policy
+        self.intra = intra
+        self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency)
+        self.comm = None
+        i = PlanInfo_t()
+        check(lib().themis_plan_info(self.h, C.byref(i)))
+        D = i.ndims
+        self.info = {
+            "ndims": D, "n_chunks": i.n_chunks, "n_ranks": i.n_ranks, "n_stages": i.n_stages,
+            "n_greedy": i.n_greedy, "time_scale": i.time_scale, "byte_scale": i.byte_scale,
+            "makespan": i.makespan, "busy": list(i.busy[:D]), "idle": list(i.idle[:D]),
+            "dim_volume": list(i.dim_volume[:D]), "final_load": list(i.final_load[:D]), "hash": i.hash,
+        }
+
+    # -- queries -------------------------------------------------------------
+    @property
+    def D(self) -> int:
+        return self.info["ndims"]
+
+    def orders(self):
+        C_, D = self.info["n_chunks"], self.D
+        rs = np.zeros(C_ * D, np.uint8)
+        ag = np.zeros(C_ * D, np.uint8)
+        check(lib().themis_plan_orders(self.h, rs.ctypes.data, ag.ctypes.data))
+        return rs.reshape(C_, D), ag.reshape(C_, D)
+
+    def dim_ops(self) -> list:
+        C_, D, NS = self.info["n_chunks"], self.D, self.info["n_stages"]
+        buf = np.zeros(D * C_ * NS, np.uint32)
+        n = np.zeros(D, np.int32)
+        check(lib().themis_plan_dim_ops(self.h, buf.ctypes.data, n.ctypes.data))
+        out = []
+        for k in range(D):
+            row = buf[k * C_ * NS: k * C_ * NS + n[k]]
+            out.append([(int(e) >> 8, int(e) & 0xFF) for e in row])
+        return out
+
+    def times(self):
+        n = self.info["n_chunks"] * self.info["n_stages"]
+        s = np.zeros(n, np.uint64)
+        e = np.zeros(n, np.uint64)
+        check(lib().themis_plan_times(self.h, s.ctypes.data, e.ctypes.data))
+        return s, e
+
+    def makespan_ns(self) -> Fraction:
+        return Fraction(self.info["makespan"], self.info["time_scale"])
+
+    # -- execution -------------------------------------------------------------
+    def bind(self, comm: "Comm", ctas_per_dim: Optional[Sequence[int]] = None) -> "Plan":
+        arr = None
+        if ctas_per_dim is not None:
+            arr = (C.c_int32 * MAX_DIMS)(*[int(x) for x in ctas_per_dim])
+        check(lib().themis_plan_bind(self.h, comm.h, arr))
+        self.comm = comm
+        return self
+
+    def bound_ctas(self) -> list:
+        arr = (C.c_int32 * MAX_DIMS)()
+        check(lib().themis_plan_bound_ctas(self.h, arr))
+        return list(arr[:self.D])
+
+    def close(self):
+        if self.h:
+            lib().themis_plan_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def heap_layout(n_ranks: int, n_gpus: int, data_bytes: int):
+    s, st, hb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    check(lib().themis_heap_layout(n_ranks, n_gpus, int(data_bytes), C.byref(s), C.byref(st), C.byref(hb)))
+    return s.value, st.value, hb.value
+
+
+class _CAI:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class Comm:
+    """Heap + peer table for the W GPUs hosting a P-rank logical topology.
+
+    Single process (group None): W = 1, all P ranks live in this GPU's HBM
+    (V = P).  Multi-process: one process per GPU in `group`; V = P / W ranks
+    per GPU; heaps are exchanged as CUDA IPC handles over the process group.
+    """
+
+    def __init__(self, topo: Topology, data_bytes: int, group=None, device=None):
+        import torch
+        self.topo = topo
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        torch.cuda.set_device(self.device)
+        if group is not None:
+            import torch.distributed as dist
+            self.W = dist.get_world_size(group)
+            self.gpu_rank = dist.get_rank(group)
+        else:
+            self.W, self.gpu_rank = 1, 0
+        if self.W > MAX_GPUS or topo.P % self.W:
+            raise ValueError(f"{topo.P} logical ranks cannot be spread over {self.W} GPUs")
+        self.P = topo.P
+        self.V = topo.P // self.W
+        self.sig_bytes, self.vrank_stride, self.heap_bytes = heap_layout(self.P, self.W, data_bytes)
+        heap = C.c_void_p()
+        check(lib().themis_heap_alloc(self.heap_bytes, C.byref(heap)))
+        self.heap = heap.value
+        self.imported = []
+        heaps = [0] * self.W
+        heaps[self.gpu_rank] = self.heap
+        if self.W > 1:
+            import torch.distributed as dist
+            h = (C.c_uint8 * IPC_HANDLE_BYTES)()
+            check(lib().themis_heap_export(self.heap, h))
+            allh = [None] * self.W
+            dist.all_gather_object(allh, bytes(h), group=group)
+            for g in range(self.W):
+                if g == self.gpu_rank:
+                    continue
+                hh = (C.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(allh[g])
+                p = C.c_void_p()
+                check(lib().themis_heap_import(hh, C.byref(p)))
+                heaps[g] = p.value
+                self.imported.append(p.value)
+        arr = (C.c_void_p * MAX_GPUS)(*heaps)
+        tc = topo.to_c()
+        out = C.c_void_p()
+        check(lib().themis_comm_create(self.gpu_rank, self.W, C.byref(tc), arr, self.heap_bytes, self.vrank_stride,
+                                       C.byref(out)))
+        self.h = out
+        self.data_ptr = self.heap + self.V * self.sig_bytes    # local rank 0's data region
+
+    def rank_view(self, v: int, count: int, dtype: str):
+        """torch view of local rank v's first `count` elements."""
+        import torch
+        ptr = self.data_ptr + v * self.vrank_stride
+        ts = {"f32": "<f4", "i32": "<i4", "f16": "<f2", "bf16": "<i2"}[dtype]
+        t = torch.as_tensor(_CAI(ptr, count, ts), device=self.device)
+        return t.view(torch.bfloat16) if dtype == "bf16" else t
+
+    def status(self) -> None:
+        check(lib().themis_comm_status(self.h))
+
+    def set_engine(self, engine: str) -> None:
+        check(lib().themis_comm_set_engine(self.h, {"ldg": 0, "tma": 1}[engine]))
+
+    def set_timeout(self, seconds: float) -> None:
+        check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
+
+    def enable_trace(self, on: bool = True) -> None:
+        check(lib().themis_comm_enable_trace(self.h, int(on)))
+
+    def fetch_trace(self, plan: Plan) -> np.ndarray:
+        n = plan.info["n_chunks"] * plan.info["n_stages"] * 2
+        out = np.zeros(n, np.uint64)
+        check(lib().themis_trace_fetch(self.h, out.ctypes.data, n))
+        return out.reshape(plan.info["n_chunks"], plan.info["n_stages"], 2)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().themis_comm_free(self.h)
+            self.h = None
+            for p in self.imported:
+                lib().themis_heap_close(p)
+            self.imported = []
+            lib().themis_heap_free(self.heap)
+            self.heap = None
+
+
+def _stream_ptr(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def themis_allreduce(buf: int, count: int, dtype: str, plan: Plan, stream=None) -> None:
+    check(lib().themis_allreduce(buf, count, DTYPES[dtype], plan.h, _stream_ptr(stream)))
+
+
+def themis_reduce_scatter(buf: int, count: int, dtype: str, plan: Plan, stream=None) -> None:
+    check(lib().themis_reduce_scatter(buf, count, DTYPES[dtype], plan.h, _stream_ptr(stream)))
+
+
+def themis_all_gather(buf: int, count: int, dtype: str, plan: Plan, stream=None) -> None:
+    check(lib().themis_all_gather(buf, count, DTYPES[dtype], plan.h, _stream_ptr(stream)))
+
+
+def themis_allreduce_host(host_in: int, host_out: int, buf: int, count: int, dtype: str, plan: Plan,
+                          stream=None) -> None:
+    check(lib().themis_allreduce_host(host_in, host_out, buf, count, DTYPES[dtype], plan.h, _stream_ptr(stream)))
+
+
+def run(coll: int, comm: Comm, plan: Plan, count: int, dtype: str, stream=None) -> None:
+    """Enqueue `coll` on the comm's data region (local rank 0 at comm.data_ptr)."""
+    fn = {ALLREDUCE: themis_allreduce, REDUCE_SCATTER: themis_reduce_scatter, ALL_GATHER: themis_all_gather}[coll]
+    fn(comm.data_ptr, count, dtype, plan, stream)
+
+
+def default_ctas(bw: Sequence[int], total: int) -> list:
+    """CTA caps per dimension proportional to bandwidth (largest remainder,
+    >= 1 each) — the bandwidth-emulation knob (north_star (d))."""
+    s = sum(bw)
+    raw = [total * b / s for b in bw]
+    n = [max(1, int(x)) for x in raw]
+    order = sorted(range(len(bw)), key=lambda k: (-(raw[k] - int(raw[k])), k))
+    i = 0
+    while sum(n) < total:
+        n[order[i % len(bw)]] += 1
+        i += 1
+    while sum(n) > total:
+        n[n.index(max(n))] -= 1
+    return n
+
+
+def launches_per_call() -> int:
+    return lib().themis_launches_per_call()
+
+
+def version() -> str:
+    return lib().themis_version().decode()
+
+
+__all__ = ["Topology", "Plan", "Comm", "themis_plan", "themis_allreduce", "themis_reduce_scatter",
+           "themis_all_gather", "themis_allreduce_host", "run", "heap_layout", "default_ctas", "ThemisError",
+           "RING", "DIRECT", "SWITCH", "ALLREDUCE", "REDUCE_SCATTER", "ALL_GATHER", "BASELINE", "THEMIS", "SCF",
+           "FIFO", "SCF_LITERAL", "DTYPES", "ELEM_SIZE"]

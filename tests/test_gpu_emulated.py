@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a executor vs the oracle, all logical ranks emulated
+inside one B200's HBM (W = 1, V = P).  Calls go through the C ABI.
+
+* int32: bit-exact vs the plain definition sum_r x_r (mod 2^32);
+* f32 / bf16 / f16: bit-exact vs the oracle run step by step with the same
+  schedule (same per-stage coordinate-order sums and rounding, R18), and
+  within the north_star tolerance of the fp64 sum (1e-5 f32, 1e-2 bf16,
+  relative to sum_r |x_r|, F10);
+* RS / AG halves against their definitions;
+* sizes span several TMA tiles per slice plus a ragged tail.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import data as O, engine as E, scheduler as S, topology as T
+from paper_2110_04478_b200 import themis as th
+from synth import ELEM_SIZE, host_inputs, torch_dtype
+
+pytestmark = pytest.mark.gpu
+
+COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
+TOL = {"f32": 1e-5, "bf16": 1e-2, "f16": 1e-3}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF):
+    o = T.Topology.make(sizes, [b for b in bw])
+    return S.schedule_collective(o, coll, nbytes, C, S.THEMIS if policy == th.THEMIS else S.BASELINE)
+
+
+def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
+             intra=th.SCF, repeat=1):
+    topo = th.Topology(tuple(sizes), tuple(bw))
+    P = topo.P
+    N = P * C * slice_elems
+    esz = ELEM_SIZE[dtype]
+    comm = th.Comm(topo, N * esz)
+    comm.set_engine(engine)
+    comm.set_timeout(10.0)
+    plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra).bind(comm, ctas)
+    try:
+        xs = host_inputs(P, N, dtype)
+        for it in range(repeat):
+            for r in range(P):
+                v = comm.rank_view(r, N, dtype)
+                src = torch.from_numpy(xs[r].view(np.int16) if dtype == "bf16" else xs[r])
+                if dtype == "bf16":
+                    src = src.view(torch.bfloat16)
+                v.copy_(src.to(v.device))
+            th.run(COLL[coll], comm, plan, N, dtype)
+            torch.cuda.synchronize()
+            comm.status()
+        outs = []
+        for r in range(P):
+            t = comm.rank_view(r, N, dtype).cpu()
+            outs.append(t.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else t.numpy())
+        return xs, outs
+    finally:
+        plan.close()
+        comm.close()
+
+
+def check_ar(sizes, bw, dtype, C, slice_elems, policy=th.THEMIS, **kw):
+    xs, outs = run_case(sizes, bw, dtype, C, slice_elems, S.AR, policy, **kw)
+    N = xs[0].shape[0]
+    P = len(xs)
+    if dtype == "i32":
+        want = O.allreduce_definition(xs, "i32")
+        for r in range(P):
+            assert np.array_equal(outs[r], want), f"rank {r}"
+        return
+    sched = oracle_sched(sizes, bw, S.AR, N * ELEM_SIZE[dtype], C, policy)
+    tree = O.run_schedule(xs, sched, dtype)
+    ref = O.allreduce_definition(xs, dtype)
+    scale = O.abs_sum(xs, dtype)
+    for r in range(P):
+        assert np.array_equal(outs[r].view(np.uint8), tree[r].view(np.uint8)), f"rank {r} not bit-exact"
+        err = np.abs(O.to_f64(outs[r], dtype) - ref)
+        assert np.all(err <= TOL[dtype] * scale)
+
+
+# slice_elems chosen so one slice spans several 32 KiB TMA tiles plus a ragged
+# (non-tile-multiple) tail: 20484 f32 = 81936 B = 2.5 tiles + 16 B.
+RAGGED = {"f32": 20484, "i32": 20484, "bf16": 40968, "f16": 40968}
+
+
+@pytest.mark.parametrize("sizes,bw", [((2,), (1,)), ((4,), (1,)), ((8,), (1,)), ((2, 2), (2, 1)), ((2, 4), (4, 1)),
+                                      ((4, 2), (1, 1)), ((2, 2, 2), (1, 1, 1)), ((2, 2, 2), (4, 2, 1)),
+                                      ((3, 2), (1, 1)), ((2, 2, 2, 2), (1, 1, 1, 1))])
+def test_allreduce_int32_exact(sizes, bw):
+    check_ar(sizes, bw, "i32", 4, RAGGED["i32"] // 4)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("policy", [th.THEMIS, th.BASELINE])
+def test_allreduce_float_bitexact_vs_oracle(dtype, policy):
+    check_ar((2, 2, 2), (1, 1, 1), dtype, 8, RAGGED[dtype], policy)
+
+
+def test_allreduce_ldg_engine():
+    check_ar((2, 2, 2), (1, 1, 1), "f32", 8, RAGGED["f32"], engine="ldg")
+    check_ar((4, 2), (1, 1), "bf16", 4, RAGGED["bf16"], engine="ldg")
+    check_ar((8,), (1,), "i32", 2, 1028, engine="ldg")
+
+
+def test_allreduce_many_chunks_and_fifo():
+    check_ar((2, 4), (1, 1), "f32", 64, 256, intra=th.FIFO)
+    check_ar((2, 2, 2), (2, 2, 1), "i32", 256, 4)
+
+
+def test_single_chunk_single_cta_per_dim():
+    check_ar((2, 2, 2), (1, 1, 1), "f32", 1, 4096, ctas=[1, 1, 1])
+
+
+def test_repeated_calls_epochs():
+    check_ar((2, 2), (1, 1), "i32", 4, 1024, repeat=3)
+
+
+@pytest.mark.parametrize("sizes", [(2, 2, 2), (4, 2), (3, 2)])
+def test_reduce_scatter_and_all_gather(sizes):
+    bw = (1,) * len(sizes)
+    C = 4
+    xs, outs = run_case(sizes, bw, "i32", C, 2048, "RS")
+    P = len(xs)
+    want = O.reduce_scatter_definition(xs, "i32", P)
+    blk = xs[0].shape[0] // P
+    for r in range(P):
+        assert np.array_equal(outs[r][r * blk:(r + 1) * blk], want[r])
+    xs, outs = run_case(sizes, bw, "i32", C, 2048, "AG")
+    cat = O.all_gather_definition(xs, P)
+    for r in range(P):
+        assert np.array_equal(outs[r], cat)
+
+
+def test_bf16_reduce_scatter_bitexact():
+    sizes, bw, C = (2, 2, 2), (1, 1, 1), 4
+    xs, outs = run_case(sizes, bw, "bf16", C, 4096, "RS")
+    N = xs[0].shape[0]
+    sched = oracle_sched(sizes, bw, "RS", N * 2, C, th.THEMIS)
+    tree = O.run_schedule(xs, sched, "bf16")
+    blk = N // 8
+    for r in range(8):
+        assert np.array_equal(outs[r][r * blk:(r + 1) * blk], tree[r][r * blk:(r + 1) * blk])
+
+
+def test_argument_errors():
+    topo = th.Topology((2, 2), (1, 1))
+    N = 4 * 4 * 64
+    comm = th.Comm(topo, N * 4)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, 4)
+    try:
+        with pytest.raises(th.ThemisError) as e:         # not bound
+            th.run(th.ALLREDUCE, comm, plan, N, "f32")
+        assert e.value.status == 6
+        plan.bind(comm)
+        with pytest.raises(th.ThemisError) as e:         # count != plan bytes
+            th.run(th.ALLREDUCE, comm, plan, N // 2, "f32")
+        assert e.value.status == 1
+        with pytest.raises(th.ThemisError) as e:         # wrong collective for the plan
+            th.run(th.REDUCE_SCATTER, comm, plan, N, "f32")
+        assert e.value.status == 6
+        with pytest.raises(th.ThemisError) as e:         # outside the heap
+            th.themis_allreduce(comm.heap + 8, N, "f32", plan)
+        assert e.value.status == 5
+        bad = th.Plan(topo, th.ALLREDUCE, 4 * 4 * 3 * 4, 4)   # 48 elements: not a multiple of P*C*4
+        bad.bind(comm)
+        with pytest.raises(th.ThemisError) as e:
+            th.run(th.ALLREDUCE, comm, bad, 48, "f32")
+        assert e.value.status == 2
+        bad.close()
+        with pytest.raises(th.ThemisError):              # too many CTAs for co-residency
+            plan.bind(comm, [1000, 1000])
+    finally:
+        plan.close()
+        comm.close()
+
+
+def test_watchdog_on_missing_peer():
+    """Fault injection: a peer that never runs its kernel
+    must not hang the GPU — the watchdog latches THEMIS_ERR_TIMEOUT."""
+    import ctypes as C
+    from paper_2110_04478_b200._lib import MAX_GPUS, check, lib
+    topo = th.Topology((2,), (1,))
+    N = 2 * 4 * 1024
+    sig, stride, hb = th.heap_layout(2, 2, N * 4)
+    h0, h1 = C.c_void_p(), C.c_void_p()
+    check(lib().themis_heap_alloc(hb, C.byref(h0)))
+    check(lib().themis_heap_alloc(hb, C.byref(h1)))        # the silent "peer"'s heap
+    heaps = (C.c_void_p * MAX_GPUS)(h0.value, h1.value)
+    comm = C.c_void_p()
+    tc = topo.to_c()
+    check(lib().themis_comm_create(0, 2, C.byref(tc), heaps, hb, stride, C.byref(comm)))
+    check(lib().themis_comm_set_timeout(comm, int(0.3e9)))
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, 4)
+    check(lib().themis_plan_bind(plan.h, comm, None))
+    buf = h0.value + sig
+    check(lib().themis_allreduce(buf, N, 0, plan.h, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    st = lib().themis_comm_status(comm)
+    assert st == 8
+    with pytest.raises(th.ThemisError) as e:                # latched: next call reports it
+        check(lib().themis_allreduce(buf, N, 0, plan.h, torch.cuda.current_stream().cuda_stream))
+    assert e.value.status == 8
+    plan.close()
+    lib().themis_comm_free(comm)
+    lib().themis_heap_free(h0)
+    lib().themis_heap_free(h1)
+
+
+def test_trace_follows_enforced_order():
+    topo = th.Topology((2, 2, 2), (1, 1, 1))
+    C_ = 8
+    N = 8 * C_ * 4096
+    comm = th.Comm(topo, N * 4)
+    comm.enable_trace(True)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm, [4, 4, 4])
+    try:
+        th.run(th.ALLREDUCE, comm, plan, N, "f32")
+        torch.cuda.synchronize()
+        tr = comm.fetch_trace(plan).astype(np.int64)
+        assert np.all(tr[:, :, 1] >= tr[:, :, 0]) and np.all(tr > 0)
+        for k, ops in enumerate(plan.dim_ops()):
+            starts = [tr[c, s, 0] for c, s in ops]
+            assert starts == sorted(starts), f"dim {k} ran out of the enforced order"
+        for c in range(C_):                             # chunk chains respected
+            for s in range(1, 6):
+                assert tr[c, s, 0] >= tr[c, s - 1, 1] - 2000   # globaltimer granularity slack
+    finally:
+        plan.close()
+        comm.close()
+
+
+def test_host_buffer_entry_point():
+    topo = th.Topology((2, 2), (1, 1))
+    C_ = 4
+    N = 4 * C_ * 1024
+    comm = th.Comm(topo, N * 4)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm)
+    try:
+        xs = host_inputs(4, N, "i32")
+        hin = torch.from_numpy(np.concatenate(xs)).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "i32", plan)
+        torch.cuda.synchronize()
+        want = O.allreduce_definition(xs, "i32")
+        for r in range(4):
+            assert np.array_equal(hout.numpy()[r * N:(r + 1) * N], want)
+    finally:
+        plan.close()
+        comm.close()

@@ -1,0 +1,157 @@
+"""Bit-exact parity: C++ planner in libthemis (through the C ABI) vs the oracle.
+
+The planner is host code, so these run without a GPU.  Compared exactly:
+per-chunk RS/AG orders, per-dimension enforced op order, every op's
+pre-simulated start/end time, makespan, busy_K, idle_K, N_K and the final Dim
+Load Tracker, after converting the oracle's rationals with the plan's
+time_scale / byte_scale.
+"""
+
+import random
+from fractions import Fraction
+
+import pytest
+
+from oracle import engine as E, scheduler as S, topology as T
+from paper_2110_04478_b200 import themis as th
+
+KINDS = {T.RING: th.RING, T.DIRECT: th.DIRECT, T.SWITCH: th.SWITCH}
+COLLS = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
+INTRA = {E.SCF: th.SCF, E.FIFO: th.FIFO, E.SCF_LITERAL: th.SCF_LITERAL}
+
+
+def make_pair(sizes, bw_mbps, kinds=None, lat=None):
+    kinds = kinds or [T.DIRECT] * len(sizes)
+    lat = lat or [0] * len(sizes)
+    o = T.Topology.make(sizes, [Fraction(b, 1000) for b in bw_mbps], kinds, lat)   # bytes/ns
+    g = th.Topology(tuple(sizes), tuple(bw_mbps), tuple(KINDS[k] for k in kinds), tuple(lat))
+    return o, g
+
+
+def compare(o_topo, g_topo, coll, nbytes, C, policy, intra, div=16, charge=False):
+    sched = S.schedule_collective(o_topo, coll, nbytes, C, policy, div)
+    m = E.simulate(sched, intra, charge_latency=charge)
+    plan = th.Plan(g_topo, COLLS[coll], nbytes, C, th.THEMIS if policy == S.THEMIS else th.BASELINE,
+                   INTRA[intra], div, charge)
+    try:
+        info = plan.info
+        ts, bs = info["time_scale"], info["byte_scale"]
+        rs, ag = plan.orders()
+        D = o_topo.D
+        for cs in sched.chunks:
+            if cs.rs:
+                assert tuple(int(x) for x in rs[cs.chunk]) == cs.rs
+            if cs.ag:
+                assert tuple(int(x) for x in ag[cs.chunk]) == cs.ag
+        assert info["n_greedy"] == sched.n_greedy
+        assert plan.dim_ops() == [list(x) for x in m.dim_order]
+        assert Fraction(info["makespan"], ts) == m.makespan
+        assert [Fraction(b, ts) for b in info["busy"]] == m.busy
+        assert [Fraction(b, ts) for b in info["idle"]] == m.idle
+        assert [Fraction(v, bs) for v in info["dim_volume"]] == m.volume
+        assert [Fraction(v, ts) for v in info["final_load"]] == sched.loads
+        st, en = plan.times()
+        NS = info["n_stages"]
+        for (c, s), t0 in m.start.items():
+            assert Fraction(int(st[c * NS + s]), ts) == t0
+            assert Fraction(int(en[c * NS + s]), ts) == m.end[(c, s)]
+        assert D == info["ndims"]
+    finally:
+        plan.close()
+
+
+def test_fig3_example():
+    o, g = make_pair((4, 4), (2000, 1000))
+    for pol in (S.BASELINE, S.THEMIS):
+        for ip in (E.FIFO, E.SCF, E.SCF_LITERAL):
+            compare(o, g, S.AR, 256 << 20, 4, pol, ip)
+
+
+@pytest.mark.parametrize("ratio", [(4, 2, 1), (1, 1, 1), (2, 2, 1)])
+def test_config2_2x2x2(ratio):
+    o, g = make_pair((2, 2, 2), [r * 100000 for r in ratio])
+    for pol in (S.BASELINE, S.THEMIS):
+        compare(o, g, S.AR, 1 << 30, 64, pol, E.SCF)
+        compare(o, g, S.AR, 1 << 30, 64, pol, E.FIFO)
+
+
+def test_config1_2x4():
+    o, g = make_pair((2, 4), (200000, 50000))
+    for pol in (S.BASELINE, S.THEMIS):
+        compare(o, g, S.AR, 64 * 1024, 4, pol, E.SCF)
+
+
+@pytest.mark.parametrize("name", sorted(T.PRESETS))
+def test_table2_topologies_1024_ranks(name):
+    t = T.PRESETS[name]
+    bw = [int(d.bw * 1000) for d in t.dims]
+    assert all(Fraction(b, 1000) == d.bw for b, d in zip(bw, t.dims))
+    o, g = make_pair(t.sizes, bw, [d.kind for d in t.dims], [int(d.step_latency) for d in t.dims])
+    for mb in (100, 1000):
+        for pol in (S.BASELINE, S.THEMIS):
+            for ip in (E.SCF, E.FIFO):
+                compare(o, g, S.AR, mb << 20, 64, pol, ip)
+    compare(o, g, S.AR, 100 << 20, 64, S.THEMIS, E.SCF, charge=True)
+
+
+def test_config5_2x8x8x8_rs_ag():
+    o, g = make_pair((2, 8, 8, 8), (300000, 175000, 150000, 100000))
+    for coll in ("RS", "AG", S.AR):
+        for mb in (4, 64, 1024):
+            compare(o, g, coll, mb << 20, 64, S.THEMIS, E.SCF)
+
+
+BWS = [12500, 25000, 50000, 100000, 150000, 175000, 200000, 250000, 300000, 375000, 400000, 450000, 900000]
+
+
+def test_random_configs():
+    rng = random.Random(20211010)
+    skipped = 0
+    for _ in range(400):
+        D = rng.randint(1, 4)
+        sizes = [rng.choice([2, 3, 4, 5, 8, 16]) for _ in range(D)]
+        kinds = [rng.choice([T.RING, T.DIRECT, T.SWITCH]) if s & (s - 1) == 0 else rng.choice([T.RING, T.DIRECT])
+                 for s in sizes]
+        bw = [rng.choice(BWS) if rng.random() < 0.7 else rng.randint(1, 12) for _ in range(D)]
+        lat = [rng.choice([0, rng.randint(0, 3000)]) for _ in range(D)]
+        o, g = make_pair(sizes, bw, kinds, lat)
+        coll = rng.choice([S.AR, S.AR, "RS", "AG"])
+        nbytes = rng.randint(1, 1 << 22) * rng.choice([1, 4096])
+        try:
+            compare(o, g, coll, nbytes, rng.randint(1, 48), rng.choice([S.BASELINE, S.THEMIS]),
+                    rng.choice([E.SCF, E.FIFO, E.SCF_LITERAL]), rng.choice([16, 16, rng.randint(1, 100)]),
+                    rng.random() < 0.2)
+        except th.ThemisError as e:      # exact 64-bit outputs cannot hold this plan
+            assert e.status == 4
+            skipped += 1
+    assert skipped < 40
+
+
+def test_plan_validation_errors():
+    with pytest.raises(th.ThemisError) as e:
+        th.Plan(th.Topology((1, 4), (1, 1)), th.ALLREDUCE, 1024, 4)
+    assert e.value.status == 1
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((6,), (1,), (th.SWITCH,)), th.ALLREDUCE, 1024, 4)
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 0, 4)
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1024, 0)
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2, 2), (1, 0)), th.ALLREDUCE, 1024, 4)
+
+
+def test_overflow_is_reported():
+    # pairwise-coprime bandwidths make lcm * P * C exceed the 64-bit outputs
+    g = th.Topology((16, 16, 16, 16), (999983, 999979, 999961, 999959))
+    with pytest.raises(th.ThemisError) as e:
+        th.Plan(g, th.ALLREDUCE, 1 << 40, 1024)
+    assert e.value.status == 4
+
+
+def test_plan_hash_deterministic():
+    g = th.Topology((2, 2, 2), (1, 1, 1))
+    a = th.Plan(g, th.ALLREDUCE, 1 << 30, 64)
+    b = th.Plan(g, th.ALLREDUCE, 1 << 30, 64)
+    c = th.Plan(g, th.ALLREDUCE, 1 << 30, 64, policy=th.BASELINE)
+    assert a.info["hash"] == b.info["hash"] != c.info["hash"]
