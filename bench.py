@@ -1,0 +1,404 @@
+"""Benchmark: Themis chunked hierarchical All-Reduce on B200 (BASELINE.json).
+
+    python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
+    python bench.py --impl reference [...]                      # the CPU oracle arm
+
+Workload (BASELINE.json configs[1]): logical 2x2x2 topology (P = 8 ranks),
+1 GiB fp32 per rank, 64 chunks, per-dimension bandwidth emulated 4:2:1 by
+capping each dimension group's CTAs.  With N GPUs each GPU hosts V = 8 / N
+logical ranks (N = 1: the whole topology inside one GPU's HBM; N = 8: one rank
+per GPU, every dimension over NVLink).  A step is one All-Reduce through the
+C ABI (one kernel launch).  Before every step the inputs are refreshed from a
+pristine copy (untimed; writes 8 GiB > L2).  `value` = bus GB/s per logical
+rank, 2 S (P-1)/P / t (NCCL-tests convention; comparable to 900 GB/s
+NVLink), t = max over GPUs of the device-timed step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "All-Reduce bus GB/s vs 900 GB/s NVLink at 2/4/8 B200, Themis vs baseline order"
+SIZES = (2, 2, 2)
+NVLINK_PEAK = 770.0       # measured peer-copy GB/s per direction (B200_PROFILING.md; 900 nominal)
+
+
+def logical_layout(sizes, n_gpus):
+    """V ranks per GPU; dims whose peers live on other GPUs (dim1 fastest)."""
+    P = 1
+    for s in sizes:
+        P *= s
+    V = P // n_gpus
+    cross, stride = [], 1
+    for k, s in enumerate(sizes):
+        if stride * s > V or stride >= V:   # peers differ in a digit at or above V's span
+            cross.append(k)
+        stride *= s
+    return {"P": P, "V": V, "cross_gpu_dims": cross}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        try:
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+        except Exception:
+            pass
+
+    def __enter__(self):
+        try:   # a persistent sampler (-lms 50) started before the timed region
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(5)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) > 8 for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def hbm_bytes_per_rank(plan, S):
+    """Algorithmic HBM bytes one rank's ops move (reads + writes): RS stage
+    holding H on dim k reads H (P_k pieces of H/P_k) and writes H/P_k; AG
+    stage holding h reads and writes (P_k-1) h."""
+    rs, _ = plan.orders()
+    C = plan.info["n_chunks"]
+    tot = 0.0
+    for c in range(C):
+        h = S / C
+        hist = []
+        for d in rs[c]:
+            p = SIZES[int(d)]
+            tot += h + h / p
+            h /= p
+            hist.append(p)
+        for p in reversed(hist):
+            tot += 2 * (p - 1) * h
+            h *= p
+    return tot
+
+
+def nvlink_bytes_per_rank(plan, cross):
+    """Bytes a rank pulls from other GPUs: N_K over the cross-GPU dims."""
+    vol = plan.info["dim_volume"]
+    return sum(vol[k] for k in cross) / plan.info["byte_scale"]
+
+
+def run_themis(a):
+    import torch
+    from paper_2110_04478_b200 import themis as th
+    from paper_2110_04478_b200.dist import barrier, init_from_env, max_over_ranks
+    from synth import device_input
+
+    rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lay = logical_layout(SIZES, world)
+    P, V = lay["P"], lay["V"]
+    S = a.mib << 20
+    N = S // 4
+    ratio = tuple(int(x) for x in a.ratio.split(":"))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    total_ctas = a.ctas_total or sms
+    topo = th.Topology(SIZES, ratio)
+    comm = th.Comm(topo, S, group=group, device=local)
+    comm.set_timeout(30.0)
+    pristine = [device_input(rank * V + v, N, "f32", dev) for v in range(V)]
+
+    def refill():
+        for v in range(V):
+            comm.rank_view(v, N, "f32").copy_(pristine[v])
+
+    def make(pol, rat, total_gbs=None):
+        # total_gbs: absolute per-rank bandwidth budget split in the ratio (paced
+        # emulation); otherwise the ratio itself (only ratios matter to the plan).
+        bw = tuple(int(round(r * total_gbs * 1000 / sum(rat))) for r in rat) if total_gbs else rat
+        t = th.Topology(SIZES, bw)
+        p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO)
+        p.bind(comm, th.default_ctas(rat, total_ctas))
+        return p
+
+    def timed(plan, steps, warmup):
+        for _ in range(warmup):
+            refill()
+            th.run(th.ALLREDUCE, comm, plan, N, "f32")
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            refill()
+            barrier(group, dev)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            th.run(th.ALLREDUCE, comm, plan, N, "f32")
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        comm.status()
+        mean = sum(ts) / len(ts)
+        return max_over_ranks(mean, group, dev), max_over_ranks(min(ts), group, dev)
+
+    busbw = lambda t: 2 * S * (P - 1) / P / t / 1e9
+
+    main = make(th.THEMIS, ratio)
+    clocks = ClockSampler(local)
+    with clocks:
+        t_main, t_best = timed(main, a.steps, a.warmup)
+    launches = a.steps * th.launches_per_call()
+
+    # Themis vs baseline order under the emulated ratios
+    compare = {}
+    pace_gbs = a.pace_gbs or {1: 240, 2: 240, 4: 480, 8: 720}.get(world, 240)
+    if not a.no_compare:
+        for mode in ("caps", "paced"):
+            comm.set_pacing(mode == "paced")
+            for rat in ([ratio, (1, 1, 1), (2, 2, 1)] if a.ratio == "4:2:1" else [ratio]):
+                row = {}
+                for pol, name in ((th.BASELINE, "baseline"), (th.THEMIS, "themis")):
+                    reuse = mode == "caps" and pol == th.THEMIS and rat == ratio
+                    p = main if reuse else make(pol, rat, pace_gbs if mode == "paced" else None)
+                    tt = t_main if reuse else timed(p, max(2, min(a.steps, 5)), 1)[0]
+                    row[name] = {"bus_gbs": round(busbw(tt), 1), "ms": round(tt * 1e3, 3),
+                                 "model_makespan_ns": float(p.makespan_ns()), "ctas": p.bound_ctas()}
+                    if mode == "paced":   # the paper's utilisation: busBW / sum BW (F2)
+                        row[name]["util"] = round(busbw(tt) / pace_gbs, 4)
+                    if not reuse:
+                        p.close()
+                row["measured_speedup"] = round(row["baseline"]["ms"] / row["themis"]["ms"], 3)
+                row["model_speedup"] = round(row["baseline"]["model_makespan_ns"] /
+                                             row["themis"]["model_makespan_ns"], 4)
+                if mode == "paced":
+                    row["sum_bw_gbs"] = pace_gbs
+                    # the plan's makespan is in real ns here (absolute bw): model busBW / sum BW
+                    row["model_util"] = {n: round(busbw(row[n]["model_makespan_ns"] * 1e-9) / pace_gbs, 4)
+                                         for n in ("baseline", "themis")}
+                compare[f"{mode} {':'.join(map(str, rat))}"] = row
+        comm.set_pacing(False)
+
+    # NCCL all_reduce on the same bytes (context row, N > 1 only)
+    nccl = None
+    if world > 1 and not a.no_compare:
+        import torch.distributed as dist
+        x = pristine[0].clone()
+        for _ in range(2):
+            dist.all_reduce(x)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            dist.all_reduce(x)
+        e1.record()
+        torch.cuda.synchronize()
+        tn = max_over_ranks(e0.elapsed_time(e1) / 5e3, group, dev)
+        nccl = {"bus_gbs": round(2 * S * (world - 1) / world / tn / 1e9, 1), "ranks": world,
+                "note": "torch.distributed.all_reduce (NCCL), flat over the N GPUs, same bytes per GPU; context"}
+        del x
+
+    # e2e through the C ABI with pinned HOST buffers (H2D + AR + D2H timed)
+    e2e = None
+    if not a.no_e2e:
+        hin = torch.empty(V * N, dtype=torch.float32, pin_memory=True)
+        for v in range(V):
+            hin[v * N:(v + 1) * N].copy_(pristine[v])
+        hout = torch.empty_like(hin, pin_memory=True)
+        th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "f32", main)
+        torch.cuda.synchronize()
+        k = max(1, min(a.steps, 3))
+        barrier(group, dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "f32", main)
+        e1.record()
+        torch.cuda.synchronize()
+        te = max_over_ranks(e0.elapsed_time(e1) / 1e3 / k, group, dev)
+        comm.status()
+        e2e = {"value": round(busbw(te), 2), "unit": "GB/s", "h2d_bytes_per_step": V * S, "d2h_bytes_per_step": V * S,
+               "ms_per_step": round(te * 1e3, 3)}
+        del hin, hout
+
+    # roofline of the dominant (only) kernel
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_bytes = V * hbm_bytes_per_rank(main, S)
+    nvl_bytes = V * nvlink_bytes_per_rank(main, lay["cross_gpu_dims"])
+    hbm_ach = hbm_bytes / t_main / 1e9
+    nvl_ach = nvl_bytes / t_main / 1e9
+    if world == 1 or hbm_ach / hbm_peak >= nvl_ach / NVLINK_PEAK:
+        roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_ach / hbm_peak, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": hbm_bytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+    else:
+        roof = {"bound": "nvlink", "achieved": round(nvl_ach, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
+                "frac": round(nvl_ach / NVLINK_PEAK, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": nvl_bytes,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"}
+    roof["kernel"] = "themis_exec_kernel<F32Tag,true> (TMA engine)"
+    if os.environ.get("THEMIS_TRAFFIC_JSON"):
+        try:
+            roof["traffic"] = json.load(open(os.environ["THEMIS_TRAFFIC_JSON"])).get(str(world))
+        except Exception:
+            pass
+
+    cpu = None
+    if world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(a.cpu_mib, a.chunks, ratio)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(busbw(t_main), 2), "unit": "GB/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_main * 1e3, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded U[-1,1) fp32 gradient buffers, torch generator seed 20211010+rank)",
+            "config": {"workload": "BASELINE.json configs[1]: 2x2x2 logical topology, 1 GiB fp32 All-Reduce per "
+                                   "rank, 64 chunks, emulated per-dim BW 4:2:1",
+                       "topology": "x".join(map(str, SIZES)), "bytes_per_rank": S, "chunks": a.chunks,
+                       "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
+                       "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
+                       "ctas_per_dim": main.bound_ctas(), "engine": "tma",
+                       "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
+                       "aggregate_bus_gbs": round(busbw(t_main) * P, 1),
+                       "best_step_bus_gbs": round(busbw(t_best), 2),
+                       "l2": "inputs refreshed from a pristine copy before every step (>= 1 GiB per GPU written, "
+                             "> 126 MB L2); inputs larger than L2"},
+            "clocks": clocks.summary(), "gpu_launches": launches, "roofline": roof, "e2e": e2e,
+            "compare": compare, "nccl_context": nccl, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    main.close()
+    comm.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(mib, chunks, ratio, reps=1):
+    """The oracle (as it stands) on a bounded sample of the same workload."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import data as O, scheduler as S_, topology as T
+    from synth import host_inputs
+    t = T.Topology.make(SIZES, ratio)
+    N = (mib << 20) // 4
+    xs = host_inputs(8, N, "f32")
+    sched = S_.schedule_collective(t, S_.AR, N * 4, chunks, S_.THEMIS)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        O.run_schedule(xs, sched, "f32")
+    dt = (time.perf_counter() - t0) / reps
+    P = 8
+    return {"value": round(2 * N * 4 * (P - 1) / P / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "host_cores_available": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"2x2x2 Themis All-Reduce, {mib} MiB fp32 per rank x 8 simulated ranks, {chunks} chunks, "
+                      f"numpy single-threaded, {reps} rep(s), {dt:.2f} s per All-Reduce"}
+
+
+def run_reference(a):
+    """Reference arm: the CPU oracle timed on the host, same metric/config."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import data as O, scheduler as S_, topology as T
+    from synth import host_inputs
+    ratio = tuple(int(x) for x in a.ratio.split(":"))
+    t = T.Topology.make(SIZES, ratio)
+    N = (a.cpu_mib << 20) // 4
+    xs = host_inputs(8, N, "f32")
+    sched = S_.schedule_collective(t, S_.AR, N * 4, a.chunks, S_.THEMIS)
+    for _ in range(a.warmup):
+        O.run_schedule(xs, sched, "f32")
+    ts = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        O.run_schedule(xs, sched, "f32")
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
+    v = round(2 * N * 4 * 7 / 8 / dt / 1e9, 4)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": "BASELINE.json configs[1] (2x2x2, fp32, 64 chunks, 4:2:1) — bounded sample of "
+                                  f"{a.cpu_mib} MiB per rank on the host CPU", "topology": "2x2x2",
+                      "bytes_per_rank": N * 4, "chunks": a.chunks, "bw_ratio": a.ratio},
+           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{a.cpu_mib} MiB fp32 per rank x 8 simulated ranks per step"},
+           "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="themis", choices=["themis", "reference"])
+    ap.add_argument("--mib", type=int, default=1024, help="All-Reduce bytes per logical rank (MiB)")
+    ap.add_argument("--chunks", type=int, default=64)
+    ap.add_argument("--ratio", default="4:2:1", help="emulated BW(dim1):BW(dim2):BW(dim3)")
+    ap.add_argument("--ctas-total", type=int, default=0, help="CTAs split over the dims (default: all SMs)")
+    ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")
+    ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
+    ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3 and a.impl == "themis":
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_themis(a)
+
+
+if __name__ == "__main__":
+    main()

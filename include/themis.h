@@ -173,6 +173,11 @@ themis_status_t themis_comm_status(themis_comm_t* comm);
  * into a shared-memory ring + warp-specialised reduction; 0 = per-thread
  * 16-byte LDG/STG.  Env THEMIS_COPY_ENGINE=ldg|tma sets the default. */
 themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
+/* Bandwidth emulation by pacing (TMA engine): when on, every CTA of dim k's
+ * group pulls peer bytes no faster than V * bw_mbps[k] / ctas[k], so dim k's
+ * per-rank rate is capped at the bound plan topology's absolute bw_mbps[k]
+ * (B_K = 1/BW_K).  Off (default): only the CTA caps limit it. */
+themis_status_t themis_comm_set_pacing(themis_comm_t* comm, int32_t on);
 /* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */
 themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
 /* Trace: when enabled, each dim group records %globaltimer start/end of every

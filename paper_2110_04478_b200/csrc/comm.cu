@@ -74,6 +74,7 @@ struct KParams {
   uint32_t* herr;           // host-mapped error word
   uint64_t timeout_ns;
   uint64_t* trace;          // [C*NS*2] or null
+  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
 };
 
 __device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
@@ -219,12 +220,23 @@ __device__ void run_op_tma(const KParams& p, const OpDesc& d, int gi, int gn, ch
   if (warp == 0) {
     if (lane != 0) return;
     dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy
+    // Bandwidth emulation by pacing: this CTA may pull peer bytes of this op
+    // no faster than V * BW_k / c_k (the bound topology's bw, R6).
+    const float pace = p.pace_ns_per_byte[k];
+    const uint64_t t_op = pace > 0.f ? dev::globaltimer() : 0;
+    double sent = 0.0;
     for (uint64_t it = u0 / Lb; it * Lb < u1; ++it) {
       const Item m = decode_item(p, d, it);
       const uint64_t a = (u0 > it * Lb ? u0 - it * Lb : 0);
       const uint64_t e = (u1 - it * Lb < Lb ? u1 - it * Lb : Lb);
       for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
         const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
+        if (pace > 0.f) {
+          const uint64_t due = t_op + (uint64_t)(sent * pace);
+          while (dev::globaltimer() < due) {
+          }
+          sent += (double)bytes * (d.phase == 0 ? pk - 1 : 1);
+        }
         const int s = ctr % kStages;
         dev::mbar_wait(&empty[s], ((ctr / kStages) & 1) ^ 1);
         dev::mbar_expect_tx(&full[s], bytes * nsrc);
@@ -393,6 +405,7 @@ struct themis_comm {
   uint32_t* herr_dev = nullptr;
   uint64_t* trace = nullptr;
   bool trace_on = false;
+  bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -525,6 +538,11 @@ extern "C" themis_status_t themis_comm_status(themis_comm_t* c) {
 extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engine) {
   if (!c || engine < 0 || engine > 1) return fail(THEMIS_ERR_INVALID_ARG, "engine must be 0 (LDG) or 1 (TMA)");
   c->engine = engine;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_pacing(themis_comm_t* c, int32_t on) {
+  if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
+  c->pacing = on != 0;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_timeout(themis_comm_t* c, uint64_t ns) {
@@ -711,6 +729,9 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.herr = c->herr_dev;
   kp.timeout_ns = c->timeout_ns;
   kp.trace = c->trace_on ? c->trace : nullptr;
+  for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
+    kp.pace_ns_per_byte[k] =
+        c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
 
   void* args[] = {&kp};
   const void* fn = kernel_for(dtype, c->engine);

@@ -191,11 +191,10 @@ class Comm:
         heaps = [0] * self.W
         heaps[self.gpu_rank] = self.heap
         if self.W > 1:
-            import torch.distributed as dist
+            from .dist import allgather_bytes
             h = (C.c_uint8 * IPC_HANDLE_BYTES)()
             check(lib().themis_heap_export(self.heap, h))
-            allh = [None] * self.W
-            dist.all_gather_object(allh, bytes(h), group=group)
+            allh = allgather_bytes(bytes(h), group)
             for g in range(self.W):
                 if g == self.gpu_rank:
                     continue
@@ -225,6 +224,10 @@ class Comm:
 
     def set_engine(self, engine: str) -> None:
         check(lib().themis_comm_set_engine(self.h, {"ldg": 0, "tma": 1}[engine]))
+
+    def set_pacing(self, on: bool) -> None:
+        """Cap each dim at its topology bw_mbps by pacing (BW emulation)."""
+        check(lib().themis_comm_set_pacing(self.h, int(on)))
 
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))

@@ -1,0 +1,93 @@
+"""Multi-GPU parity worker (one process per GPU; launched by test_gpu_multi.py
+with torchrun).  Every rank checks its own logical ranks against the oracle."""
+
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import data as O, scheduler as S, topology as T  # noqa: E402
+from paper_2110_04478_b200 import themis as th  # noqa: E402
+from paper_2110_04478_b200.dist import init_from_env  # noqa: E402
+from synth import ELEM_SIZE, host_inputs  # noqa: E402
+
+COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
+
+
+def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine):
+    topo = th.Topology(sizes, bw)
+    P = topo.P
+    V = P // W
+    N = P * C * slice_elems
+    esz = ELEM_SIZE[dtype]
+    comm = th.Comm(topo, N * esz, group=group)
+    comm.set_engine(engine)
+    comm.set_timeout(20.0)
+    plan = th.Plan(topo, COLL[coll], N * esz, C, policy).bind(comm)
+    xs = host_inputs(P, N, dtype)
+    for v in range(V):
+        r = g * V + v
+        src = torch.from_numpy(xs[r].view(np.int16) if dtype == "bf16" else xs[r])
+        view = comm.rank_view(v, N, dtype)
+        view.copy_(src.view(torch.bfloat16) if dtype == "bf16" else src)
+    torch.cuda.synchronize()
+    th.run(COLL[coll], comm, plan, N, dtype)
+    torch.cuda.synchronize()
+    comm.status()
+    o = T.Topology.make(sizes, bw)
+    sched = S.schedule_collective(o, coll, N * esz, C, S.THEMIS if policy == th.THEMIS else S.BASELINE)
+    want = O.run_schedule(xs, sched, dtype)
+    bad = []
+    blk = N // P
+    for v in range(V):
+        r = g * V + v
+        t = comm.rank_view(v, N, dtype).cpu()
+        got = t.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else t.numpy()
+        if coll == "RS":
+            ok = np.array_equal(got[r * blk:(r + 1) * blk], want[r][r * blk:(r + 1) * blk])
+        else:
+            ok = np.array_equal(got, want[r])
+        if not ok:
+            bad.append(r)
+    plan.close()
+    comm.close()
+    return bad
+
+
+def main():
+    rank, W, local, group = init_from_env("nccl")
+    cases = []
+    for engine in ("tma", "ldg"):
+        cases += [((2, 2, 2), (1, 1, 1), "i32", 8, 2052, S.AR, th.THEMIS, engine),
+                  ((2, 2, 2), (4, 2, 1), "f32", 8, 5124, S.AR, th.BASELINE, engine)]
+    cases += [((2, 2, 2), (1, 1, 1), "bf16", 4, 8200, S.AR, th.THEMIS, "tma"),
+              ((2, 2, 2), (2, 2, 1), "f16", 64, 264, S.AR, th.THEMIS, "tma"),
+              ((2, 2, 2), (1, 1, 1), "i32", 4, 2048, "RS", th.THEMIS, "tma"),
+              ((2, 2, 2), (1, 1, 1), "i32", 4, 2048, "AG", th.THEMIS, "tma"),
+              ((W,), (1,), "f32", 4, 8196, S.AR, th.THEMIS, "tma"),
+              ((2, 4), (1, 1), "f32", 16, 1028, S.AR, th.THEMIS, "tma"),
+              ((4, 2), (1, 1), "i32", 16, 1028, S.AR, th.THEMIS, "tma")]
+    fails = []
+    for c in cases:
+        if int(np.prod(c[0])) % W:
+            continue
+        bad = case(group, W, rank, *c)
+        if bad:
+            fails.append((c, bad))
+    import torch.distributed as dist
+    t = torch.tensor([len(fails)], device="cuda")
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"mp_worker W={W}: {len(cases)} cases, failing ranks total {int(t.item())}")
+    for c, bad in fails:
+        print(f"rank {rank} FAIL {c} logical ranks {bad}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

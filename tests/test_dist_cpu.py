@@ -1,0 +1,57 @@
+"""World-size-2 gloo tests (CPU) of the multi-process host logic: IPC-handle
+exchange, max-over-ranks timing, and bench.py's aggregation helpers."""
+
+import os
+import socket
+
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    from paper_2110_04478_b200.dist import allgather_bytes, barrier, init_from_env, max_over_ranks
+    r, w, local, group = init_from_env("gloo")
+    try:
+        handles = allgather_bytes(bytes([r]) * 64, group)
+        m = max_over_ranks(1.5 + r, group)
+        barrier(group)
+        q.put((r, [h[0] for h in handles], len(handles[0]), m))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_handle_exchange_and_max():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(world))
+    for r, firsts, n, m in res:
+        assert firsts == [0, 1] and n == 64 and m == 2.5
+
+
+def test_rank_layout_helpers():
+    from bench import logical_layout
+    lay = logical_layout((2, 2, 2), 4)
+    assert lay["V"] == 2 and lay["cross_gpu_dims"] == [1, 2]
+    lay = logical_layout((2, 2, 2), 2)
+    assert lay["V"] == 4 and lay["cross_gpu_dims"] == [2]
+    lay = logical_layout((2, 2, 2), 1)
+    assert lay["V"] == 8 and lay["cross_gpu_dims"] == []

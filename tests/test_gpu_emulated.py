@@ -21,7 +21,7 @@ from synth import ELEM_SIZE, host_inputs, torch_dtype
 pytestmark = pytest.mark.gpu
 
 COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
-TOL = {"f32": 1e-5, "bf16": 1e-2, "f16": 1e-3}
+TOL = {"f32": 1e-5, "bf16": 1e-2, "f16": 3 * 2.0 ** -11}   # f16: one RNE per RS stage, D = 3
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -96,7 +96,7 @@ RAGGED = {"f32": 20484, "i32": 20484, "bf16": 40968, "f16": 40968}
                                       ((4, 2), (1, 1)), ((2, 2, 2), (1, 1, 1)), ((2, 2, 2), (4, 2, 1)),
                                       ((3, 2), (1, 1)), ((2, 2, 2, 2), (1, 1, 1, 1))])
 def test_allreduce_int32_exact(sizes, bw):
-    check_ar(sizes, bw, "i32", 4, RAGGED["i32"] // 4)
+    check_ar(sizes, bw, "i32", 4, RAGGED["i32"] // 4 + 3)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
