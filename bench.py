@@ -104,6 +104,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def paced_bw(rat, total_gbs):
+    """Absolute per-dim MB/s in the exact ratio `rat`, summing to ~total_gbs,
+    on a whole-GB/s unit (keeps the planner's lcm of bandwidths small)."""
+    unit = max(1, int(round(total_gbs / sum(rat)))) * 1000
+    return tuple(int(r) * unit for r in rat)
+
+
 def hbm_bytes_per_rank(plan, S):
     """Algorithmic HBM bytes one rank's ops move (reads + writes): RS stage
     holding H on dim k reads H (P_k pieces of H/P_k) and writes H/P_k; AG
@@ -137,6 +144,7 @@ def run_themis(a):
     from paper_2110_04478_b200.dist import barrier, init_from_env, max_over_ranks
     from synth import device_input
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")      # keep stdout to the one JSON line
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
@@ -161,7 +169,7 @@ def run_themis(a):
     def make(pol, rat, total_gbs=None):
         # total_gbs: absolute per-rank bandwidth budget split in the ratio (paced
         # emulation); otherwise the ratio itself (only ratios matter to the plan).
-        bw = tuple(int(round(r * total_gbs * 1000 / sum(rat))) for r in rat) if total_gbs else rat
+        bw = paced_bw(rat, total_gbs) if total_gbs else rat
         t = th.Topology(SIZES, bw)
         p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO)
         p.bind(comm, th.default_ctas(rat, total_ctas))
@@ -203,6 +211,7 @@ def run_themis(a):
             comm.set_pacing(mode == "paced")
             for rat in ([ratio, (1, 1, 1), (2, 2, 1)] if a.ratio == "4:2:1" else [ratio]):
                 row = {}
+                sum_bw = sum(paced_bw(rat, pace_gbs)) / 1000
                 for pol, name in ((th.BASELINE, "baseline"), (th.THEMIS, "themis")):
                     reuse = mode == "caps" and pol == th.THEMIS and rat == ratio
                     p = main if reuse else make(pol, rat, pace_gbs if mode == "paced" else None)
@@ -210,16 +219,16 @@ def run_themis(a):
                     row[name] = {"bus_gbs": round(busbw(tt), 1), "ms": round(tt * 1e3, 3),
                                  "model_makespan_ns": float(p.makespan_ns()), "ctas": p.bound_ctas()}
                     if mode == "paced":   # the paper's utilisation: busBW / sum BW (F2)
-                        row[name]["util"] = round(busbw(tt) / pace_gbs, 4)
+                        row[name]["util"] = round(busbw(tt) / sum_bw, 4)
                     if not reuse:
                         p.close()
                 row["measured_speedup"] = round(row["baseline"]["ms"] / row["themis"]["ms"], 3)
                 row["model_speedup"] = round(row["baseline"]["model_makespan_ns"] /
                                              row["themis"]["model_makespan_ns"], 4)
                 if mode == "paced":
-                    row["sum_bw_gbs"] = pace_gbs
+                    row["sum_bw_gbs"] = sum_bw
                     # the plan's makespan is in real ns here (absolute bw): model busBW / sum BW
-                    row["model_util"] = {n: round(busbw(row[n]["model_makespan_ns"] * 1e-9) / pace_gbs, 4)
+                    row["model_util"] = {n: round(busbw(row[n]["model_makespan_ns"] * 1e-9) / sum_bw, 4)
                                          for n in ("baseline", "themis")}
                 compare[f"{mode} {':'.join(map(str, rat))}"] = row
         comm.set_pacing(False)

@@ -207,69 +207,87 @@ constexpr int kStageBytes = 32 * 1024;
 constexpr int kConsumerWarps = 8;
 constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8;
 
-template <class Tag>
-__device__ void run_op_tma(const KParams& p, const OpDesc& d, int gi, int gn, char* smem, uint64_t* full,
-                           uint64_t* empty, uint32_t& ctr) {
-  const int k = d.dim, pk = p.size[k];
-  const int nsrc = d.phase == 0 ? pk : 1;
-  const uint64_t Lb = p.slice_elems * p.elem_size;  // bytes per item
-  const uint64_t tot16 = op_items(p, d) * (Lb / 16);
-  const uint64_t u0 = tot16 * gi / gn * 16, u1 = tot16 * (gi + 1) / gn * 16;
-  const uint32_t tile = ((uint32_t)kStageBytes / nsrc) & ~15u;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) {
-    if (lane != 0) return;
-    dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy
-    // Bandwidth emulation by pacing: this CTA may pull peer bytes of this op
-    // no faster than V * BW_k / c_k (the bound topology's bw, R6).
-    const float pace = p.pace_ns_per_byte[k];
-    const uint64_t t_op = pace > 0.f ? dev::globaltimer() : 0;
-    double sent = 0.0;
-    for (uint64_t it = u0 / Lb; it * Lb < u1; ++it) {
-      const Item m = decode_item(p, d, it);
-      const uint64_t a = (u0 > it * Lb ? u0 - it * Lb : 0);
-      const uint64_t e = (u1 - it * Lb < Lb ? u1 - it * Lb : Lb);
-      for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
-        const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
-        if (pace > 0.f) {
-          const uint64_t due = t_op + (uint64_t)(sent * pace);
-          while (dev::globaltimer() < due) {
-          }
-          sent += (double)bytes * (d.phase == 0 ? pk - 1 : 1);
+// Geometry of op d for CTA gi of gn: byte range [u0, u1) of the op's items
+// (16-byte granules), TMA tile size per source.
+struct OpRange {
+  uint64_t u0, u1, Lb;
+  uint32_t tile;
+  int nsrc, pk;
+};
+__device__ __forceinline__ OpRange op_range(const KParams& p, const OpDesc& d, int gi, int gn) {
+  OpRange r;
+  r.pk = p.size[d.dim];
+  r.nsrc = d.phase == 0 ? r.pk : 1;
+  r.Lb = p.slice_elems * p.elem_size;
+  const uint64_t tot16 = op_items(p, d) * (r.Lb / 16);
+  r.u0 = tot16 * gi / gn * 16;
+  r.u1 = tot16 * (gi + 1) / gn * 16;
+  r.tile = ((uint32_t)kStageBytes / r.nsrc) & ~15u;
+  return r;
+}
+
+// Producer (one lane): stream the op's tiles into the shared-memory ring.
+__device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, const OpRange& r, char* smem,
+                                           uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+  const int k = d.dim;
+  dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
+  // Bandwidth emulation by pacing: this CTA pulls peer bytes of this op no
+  // faster than V * BW_k / c_k (the bound topology's bw, R6).  Due times are
+  // absolute from the op start, so timer granularity does not accumulate.
+  const float pace = p.pace_ns_per_byte[k];
+  const uint64_t t_op = pace > 0.f ? dev::globaltimer() : 0;
+  double sent = 0.0;
+  for (uint64_t it = r.u0 / r.Lb; it * r.Lb < r.u1; ++it) {
+    const Item m = decode_item(p, d, it);
+    const uint64_t a = (r.u0 > it * r.Lb ? r.u0 - it * r.Lb : 0);
+    const uint64_t e = (r.u1 - it * r.Lb < r.Lb ? r.u1 - it * r.Lb : r.Lb);
+    for (uint64_t pos = a; pos < e; pos += r.tile, ++ctr) {
+      const uint32_t bytes = (uint32_t)(e - pos < r.tile ? e - pos : r.tile);
+      if (pace > 0.f) {
+        const uint64_t due = t_op + (uint64_t)(sent * pace);
+        while (dev::globaltimer() < due) {
         }
-        const int s = ctr % kStages;
-        dev::mbar_wait(&empty[s], ((ctr / kStages) & 1) ^ 1);
-        dev::mbar_expect_tx(&full[s], bytes * nsrc);
-        char* dst = smem + s * kStageBytes;
-        if (d.phase == 0) {
-          for (int j = 0; j < pk; ++j)
-            dev::bulk_g2s(dst + j * tile, data_of(p, m.g0 + j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
-        } else {
-          dev::bulk_g2s(dst, data_of(p, m.g0 + m.j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
-        }
+        sent += (double)bytes * (d.phase == 0 ? r.pk - 1 : 1);
+      }
+      const int s = ctr % kStages;
+      dev::mbar_wait(&empty[s], ((ctr / kStages) & 1) ^ 1);
+      dev::mbar_expect_tx(&full[s], bytes * r.nsrc);
+      char* dst = smem + s * kStageBytes;
+      if (d.phase == 0) {
+        for (int j = 0; j < r.pk; ++j)
+          dev::bulk_g2s(dst + j * r.tile, data_of(p, m.g0 + j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
+      } else {
+        dev::bulk_g2s(dst, data_of(p, m.g0 + m.j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
       }
     }
-    return;
   }
-  const int ct = threadIdx.x - 32;
+}
+
+// Consumers (warps 1..kConsumerWarps): sum the P_k copies of each tile in
+// coordinate order (RS) or pass the bytes through (AG), 16-byte STG.
+// Returns false if the kernel is aborting (watchdog).
+template <class Tag>
+__device__ __forceinline__ bool consume_op(const KParams& p, const OpDesc& d, const OpRange& r, const char* smem,
+                                           uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+  const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
   constexpr int kCons = 32 * kConsumerWarps;
-  const uint32_t tile16 = tile / 16;
-  for (uint64_t it = u0 / Lb; it * Lb < u1; ++it) {
+  const uint32_t tile16 = r.tile / 16;
+  for (uint64_t it = r.u0 / r.Lb; it * r.Lb < r.u1; ++it) {
     const Item m = decode_item(p, d, it);
-    const uint64_t a = (u0 > it * Lb ? u0 - it * Lb : 0);
-    const uint64_t e = (u1 - it * Lb < Lb ? u1 - it * Lb : Lb);
+    const uint64_t a = (r.u0 > it * r.Lb ? r.u0 - it * r.Lb : 0);
+    const uint64_t e = (r.u1 - it * r.Lb < r.Lb ? r.u1 - it * r.Lb : r.Lb);
     char* base = data_of(p, m.q) + m.off;
-    for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
-      const uint32_t n16 = (uint32_t)((e - pos < tile ? e - pos : tile) / 16);
+    for (uint64_t pos = a; pos < e; pos += r.tile, ++ctr) {
+      const uint32_t n16 = (uint32_t)((e - pos < r.tile ? e - pos : r.tile) / 16);
       const int s = ctr % kStages;
-      dev::mbar_wait(&full[s], (ctr / kStages) & 1);
+      if (!dev::mbar_wait_or(&full[s], (ctr / kStages) & 1, p.abort_flag)) return false;
       const uint4* sm = reinterpret_cast<const uint4*>(smem + s * kStageBytes);
       uint4* dst = reinterpret_cast<uint4*>(base + pos);
       if (d.phase == 0) {
         for (uint32_t w = ct; w < n16; w += kCons) {
           float acc[Tag::kAcc];
           Tag::load(acc, sm[w]);
-          for (int j = 1; j < pk; ++j) Tag::add(acc, sm[j * tile16 + w]);
+          for (int j = 1; j < r.pk; ++j) Tag::add(acc, sm[j * tile16 + w]);
           dev::st_v4(dst + w, Tag::store(acc));
         }
       } else {
@@ -279,22 +297,61 @@ __device__ void run_op_tma(const KParams& p, const OpDesc& d, int gi, int gn, ch
       if (lane == 0) dev::mbar_arrive(&empty[s]);
     }
   }
+  return true;
+}
+
+// One warp: wait until the local ranks and their dim-k peers completed (c, s-1).
+__device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d, int opi) {
+  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
+  bool ok = true;
+  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
+    const int q = q0 + t / pk;
+    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+  }
+  return __all_sync(0xFFFFFFFFu, ok);
+}
+
+// One warp: count this CTA's completion of op opi; the group's last CTA
+// publishes the epoch to the consumers of (c, s): self and the next stage's
+// dim peers.  Release chain: consumers' stores -> named barrier ->
+// atom.acq_rel.gpu (all CTAs) -> fence.acq_rel.sys -> relaxed sys stores.
+__device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc& d, int opi, int gn) {
+  const int lane = threadIdx.x & 31;
+  uint32_t last = 0;
+  if (lane == 0) {
+    last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
+    if (last) {
+      p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
+      dev::fence_acq_rel_sys();
+    }
+  }
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  if (d.next_dim >= 0) {
+    const int V = p.V, q0 = p.my_gpu * V, kn = d.next_dim, pn = p.size[kn];
+    for (int t = lane; t < V * pn; t += 32) {
+      const int q = q0 + t / pn;
+      const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
+      dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
+    }
+  }
+  if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
+  __syncwarp();
 }
 
 template <class Tag, bool kTma>
 __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) char smem[];
-  __shared__ int s_flag;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int g = 0;
   while (g + 1 < p.D && (int)blockIdx.x >= p.grp_start[g + 1]) ++g;
   const int gi = blockIdx.x - p.grp_start[g];
   const int gn = p.grp_start[g + 1] - p.grp_start[g];
   const int V = p.V, P = p.P;
   const int q0 = p.my_gpu * V;
-  uint32_t ctr = 0;  // TMA ring position (identical in producer and consumers)
   bool ok = true;
   if (kTma && tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -313,46 +370,55 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
 
   // a9: walk this dimension's ops in the enforced order.
   const int* list = p.dim_ops + (uint64_t)g * p.C * p.NS;
-  for (int i = 0; ok && i < p.dim_ops_n[g]; ++i) {
-    const int opi = list[i];
-    const OpDesc& d = p.ops[opi];
-    const int k = d.dim;
-    if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
-      const int pk = p.size[k];
-      for (int t = tid; t < V * pk; t += blockDim.x) {
-        const int q = q0 + t / pk;
-        const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-        ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
-      }
-      ok = __syncthreads_and(ok);
-      if (!ok) break;
-    }
-    if (p.trace && gi == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
-    if (kTma)
-      run_op_tma<Tag>(p, d, gi, gn, smem, full, empty, ctr);
-    else
-      run_op_ldg<Tag>(p, d, gi, gn);
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence_system();
-      const uint32_t old = atomicAdd(&p.opcnt[opi], 1u);
-      s_flag = (old == (uint32_t)gn - 1);
-      if (s_flag) {
-        p.opcnt[opi] = 0;  // every CTA of the group arrived; reset for the next call
-        dev::fence_acq_rel_sys();
-      }
-    }
-    __syncthreads();
-    if (s_flag) {
-      if (d.next_dim >= 0) {  // publish (c, s) to self and to the next stage's dim peers
-        const int kn = d.next_dim, pn = p.size[kn];
-        for (int t = tid; t < V * pn; t += blockDim.x) {
-          const int q = q0 + t / pn;
-          const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
-          dev::st_release_sys(ready_slot(p, dst, q, opi), p.epoch);
+  const int nops = ok ? p.dim_ops_n[g] : 0;
+  if constexpr (kTma) {
+    // Warp-specialised and decoupled: the producer warp waits for an op's
+    // dependencies and streams its tiles, then moves on to the next op while
+    // the consumer warps finish; the consumers count and publish completion.
+    uint32_t ctr = 0;  // ring position (identical sequence in producer and consumers)
+    if (warp == 0) {
+      for (int i = 0; i < nops; ++i) {
+        const int opi = list[i];
+        const OpDesc& d = p.ops[opi];
+        const OpRange r = op_range(p, d, gi, gn);
+        if (r.u0 >= r.u1) continue;  // no bytes for this CTA: nothing to wait for
+        if (d.stage > 0 && !wait_deps_warp(p, d, opi)) break;
+        if (lane == 0) {
+          if (p.trace && gi == 0) p.trace[2 * opi] = dev::globaltimer();
+          produce_op(p, d, r, smem, full, empty, ctr);
         }
+        __syncwarp();
       }
-      if (p.trace && tid == 0) p.trace[2 * opi + 1] = dev::globaltimer();
+    } else {
+      for (int i = 0; i < nops; ++i) {
+        const int opi = list[i];
+        const OpDesc& d = p.ops[opi];
+        const OpRange r = op_range(p, d, gi, gn);
+        if (!consume_op<Tag>(p, d, r, smem, full, empty, ctr)) break;
+        dev::named_bar_sync(1, 32 * kConsumerWarps);  // all consumer stores of this op issued
+        if (warp == 1) complete_op_warp(p, d, opi, gn);
+      }
+    }
+  } else {
+    for (int i = 0; ok && i < nops; ++i) {
+      const int opi = list[i];
+      const OpDesc& d = p.ops[opi];
+      const int k = d.dim;
+      if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
+        const int pk = p.size[k];
+        for (int t = tid; t < V * pk; t += blockDim.x) {
+          const int q = q0 + t / pk;
+          const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+        }
+        ok = __syncthreads_and(ok);
+        if (!ok) break;
+      }
+      if (p.trace && gi == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
+      run_op_ldg<Tag>(p, d, gi, gn);
+      __syncthreads();
+      if (warp == 0) complete_op_warp(p, d, opi, gn);
+      __syncthreads();
     }
   }
 
