@@ -205,11 +205,17 @@ def run_themis(a):
 
     # Themis vs baseline order under the emulated ratios
     compare = {}
-    pace_gbs = a.pace_gbs or {1: 240, 2: 240, 4: 480, 8: 720}.get(world, 240)
+    # Paced budget per rank that this box can carry: NVLink (~700 GB/s per GPU
+    # over the cross-GPU dims' share) and HBM (~6 TB/s at ~2.5 B per bus byte).
+    ncross = len(lay["cross_gpu_dims"])
+    caps_ = [720.0, 6000.0 / (2.5 * V)]
+    if ncross:
+        caps_.append(700.0 * len(SIZES) / (V * ncross))
+    pace_gbs = a.pace_gbs or float(int(min(caps_) // 24) * 24)
     if not a.no_compare:
         for mode in ("caps", "paced"):
             comm.set_pacing(mode == "paced")
-            for rat in ([ratio, (1, 1, 1), (2, 2, 1)] if a.ratio == "4:2:1" else [ratio]):
+            for rat in [ratio] + [r for r in a.compare if r != ratio]:
                 row = {}
                 sum_bw = sum(paced_bw(rat, pace_gbs)) / 1000
                 for pol, name in ((th.BASELINE, "baseline"), (th.THEMIS, "themis")):
@@ -309,8 +315,11 @@ def run_themis(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_main * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded U[-1,1) fp32 gradient buffers, torch generator seed 20211010+rank)",
-            "config": {"workload": "BASELINE.json configs[1]: 2x2x2 logical topology, 1 GiB fp32 All-Reduce per "
-                                   "rank, 64 chunks, emulated per-dim BW 4:2:1",
+            "config": {"workload": ("BASELINE.json configs[1]: 2x2x2 logical topology, 1 GiB fp32 All-Reduce per "
+                                    "rank, 64 chunks, emulated per-dim BW 4:2:1")
+                       if (SIZES == (2, 2, 2) and a.ratio == "4:2:1" and a.mib == 1024 and a.chunks == 64) else
+                       (f"BASELINE.json configs[2] sweep point: {'x'.join(map(str, SIZES))}, {a.mib} MiB fp32 per "
+                        f"rank, {a.chunks} chunks, emulated BW {a.ratio}"),
                        "topology": "x".join(map(str, SIZES)), "bytes_per_rank": S, "chunks": a.chunks,
                        "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
@@ -337,18 +346,18 @@ def cpu_baseline(mib, chunks, ratio, reps=1):
     from oracle import data as O, scheduler as S_, topology as T
     from synth import host_inputs
     t = T.Topology.make(SIZES, ratio)
+    P = t.P
     N = (mib << 20) // 4
-    xs = host_inputs(8, N, "f32")
+    xs = host_inputs(P, N, "f32")
     sched = S_.schedule_collective(t, S_.AR, N * 4, chunks, S_.THEMIS)
     t0 = time.perf_counter()
     for _ in range(reps):
         O.run_schedule(xs, sched, "f32")
     dt = (time.perf_counter() - t0) / reps
-    P = 8
     return {"value": round(2 * N * 4 * (P - 1) / P / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
             "host_cores_available": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": f"2x2x2 Themis All-Reduce, {mib} MiB fp32 per rank x 8 simulated ranks, {chunks} chunks, "
-                      f"numpy single-threaded, {reps} rep(s), {dt:.2f} s per All-Reduce"}
+            "sample": f"{'x'.join(map(str, SIZES))} Themis All-Reduce, {mib} MiB fp32 per rank x {P} simulated "
+                      f"ranks, {chunks} chunks, numpy single-threaded, {reps} rep(s), {dt:.2f} s per All-Reduce"}
 
 
 def run_reference(a):
@@ -361,8 +370,9 @@ def run_reference(a):
     from synth import host_inputs
     ratio = tuple(int(x) for x in a.ratio.split(":"))
     t = T.Topology.make(SIZES, ratio)
+    P = t.P
     N = (a.cpu_mib << 20) // 4
-    xs = host_inputs(8, N, "f32")
+    xs = host_inputs(P, N, "f32")
     sched = S_.schedule_collective(t, S_.AR, N * 4, a.chunks, S_.THEMIS)
     for _ in range(a.warmup):
         O.run_schedule(xs, sched, "f32")
@@ -372,15 +382,15 @@ def run_reference(a):
         O.run_schedule(xs, sched, "f32")
         ts.append(time.perf_counter() - t0)
     dt = sum(ts) / len(ts)
-    v = round(2 * N * 4 * 7 / 8 / dt / 1e9, 4)
+    v = round(2 * N * 4 * (P - 1) / P / dt / 1e9, 4)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": "BASELINE.json configs[1] (2x2x2, fp32, 64 chunks, 4:2:1) — bounded sample of "
-                                  f"{a.cpu_mib} MiB per rank on the host CPU", "topology": "2x2x2",
+                                  f"{a.cpu_mib} MiB per rank on the host CPU", "topology": "x".join(map(str, SIZES)),
                       "bytes_per_rank": N * 4, "chunks": a.chunks, "bw_ratio": a.ratio},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                            "sample": f"{a.cpu_mib} MiB fp32 per rank x 8 simulated ranks per step"},
+                            "sample": f"{a.cpu_mib} MiB fp32 per rank x {P} simulated ranks per step"},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -400,7 +410,16 @@ def main():
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")
+    ap.add_argument("--compare-ratios", default="", help="extra emulated ratios, e.g. '1:1:1,2:2:1'")
     a = ap.parse_args()
+    global SIZES
+    SIZES = tuple(int(x) for x in a.sizes.split(","))
+    if len(a.ratio.split(":")) != len(SIZES):
+        a.ratio = ":".join(["1"] * len(SIZES))
+    if not a.compare_ratios:
+        a.compare_ratios = {3: "1:1:1,2:2:1", 2: "1:1", 1: ""}.get(len(SIZES), "")
+    a.compare = [tuple(int(x) for x in r.split(":")) for r in a.compare_ratios.split(",") if r]
     if a.warmup < 3 and a.impl == "themis":
         a.warmup = 3
     if a.impl == "reference":
