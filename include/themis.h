@@ -178,6 +178,9 @@ themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
  * per-rank rate is capped at the bound plan topology's absolute bw_mbps[k]
  * (B_K = 1/BW_K).  Off (default): only the CTA caps limit it. */
 themis_status_t themis_comm_set_pacing(themis_comm_t* comm, int32_t on);
+/* TMA ring depth per CTA, 1..6 stages of 32 KiB (bytes in flight per CTA);
+ * default 6, env THEMIS_STAGES.  Errors: INVALID_ARG. */
+themis_status_t themis_comm_set_stages(themis_comm_t* comm, int32_t stages);
 /* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */
 themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
 /* Trace: when enabled, each dim group records %globaltimer start/end of every

@@ -25,7 +25,7 @@ using namespace themis;
 
 namespace {
 
-constexpr int kThreads = 288;  // 1 producer warp + 8 consumer warps (TMA path); all 9 warps copy in the LDG path
+constexpr int kThreads = 320;  // TMA path: producer warp + 8 consumer warps + completion warp; LDG: all copy
 constexpr int kMaxRanks = 64;                                       // logical ranks a comm may host
 constexpr int kMaxOps = THEMIS_MAX_CHUNKS * 2 * THEMIS_MAX_DIMS;    // ops per plan
 constexpr uint64_t kAlign = 1ull << 16;
@@ -75,6 +75,7 @@ struct KParams {
   uint64_t timeout_ns;
   uint64_t* trace;          // [C*NS*2] or null
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
+  int32_t stages;           // TMA ring depth in use (<= kStages): bytes in flight per CTA
 };
 
 __device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
@@ -205,7 +206,9 @@ __device__ void run_op_ldg(const KParams& p, const OpDesc& d, int gi, int gn) {
 constexpr int kStages = 6;
 constexpr int kStageBytes = 32 * 1024;
 constexpr int kConsumerWarps = 8;
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8;
+constexpr int kOpRing = 16;  // ops the consumers may run ahead of the completion warp
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * (kStages + kOpRing) * 8;
+static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + completion warp");
 
 // Geometry of op d for CTA gi of gn: byte range [u0, u1) of the op's items
 // (16-byte granules), TMA tile size per source.
@@ -249,8 +252,8 @@ __device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, co
         }
         sent += (double)bytes * (d.phase == 0 ? r.pk - 1 : 1);
       }
-      const int s = ctr % kStages;
-      dev::mbar_wait(&empty[s], ((ctr / kStages) & 1) ^ 1);
+      const int s = ctr % p.stages;
+      dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
       dev::mbar_expect_tx(&full[s], bytes * r.nsrc);
       char* dst = smem + s * kStageBytes;
       if (d.phase == 0) {
@@ -279,8 +282,8 @@ __device__ __forceinline__ bool consume_op(const KParams& p, const OpDesc& d, co
     char* base = data_of(p, m.q) + m.off;
     for (uint64_t pos = a; pos < e; pos += r.tile, ++ctr) {
       const uint32_t n16 = (uint32_t)((e - pos < r.tile ? e - pos : r.tile) / 16);
-      const int s = ctr % kStages;
-      if (!dev::mbar_wait_or(&full[s], (ctr / kStages) & 1, p.abort_flag)) return false;
+      const int s = ctr % p.stages;
+      if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
       const uint4* sm = reinterpret_cast<const uint4*>(smem + s * kStageBytes);
       uint4* dst = reinterpret_cast<uint4*>(base + pos);
       if (d.phase == 0) {
@@ -345,6 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
   extern __shared__ __align__(128) char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
+  uint64_t* op_done = empty + kStages;
+  uint64_t* op_free = op_done + kOpRing;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int g = 0;
   while (g + 1 < p.D && (int)blockIdx.x >= p.grp_start[g + 1]) ++g;
@@ -357,6 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     for (int s = 0; s < kStages; ++s) {
       dev::mbar_init(&full[s], 1);
       dev::mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < kOpRing; ++s) {
+      dev::mbar_init(&op_done[s], kConsumerWarps);
+      dev::mbar_init(&op_free[s], 1);
     }
     dev::fence_mbar_init();
   }
@@ -389,14 +398,35 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         }
         __syncwarp();
       }
-    } else {
+    } else if (warp <= kConsumerWarps) {
+      // consumers: per op, every consumer warp arrives on op_done[slot]
+      // (mbarrier arrive = release.cta of its stores) once it is done, after
+      // the completion warp has freed that slot (ring of kOpRing ops).
       for (int i = 0; i < nops; ++i) {
         const int opi = list[i];
         const OpDesc& d = p.ops[opi];
         const OpRange r = op_range(p, d, gi, gn);
         if (!consume_op<Tag>(p, d, r, smem, full, empty, ctr)) break;
-        dev::named_bar_sync(1, 32 * kConsumerWarps);  // all consumer stores of this op issued
-        if (warp == 1) complete_op_warp(p, d, opi, gn);
+        __syncwarp();
+        bool w = true;
+        if (lane == 0) {
+          const int slot = i % kOpRing;
+          w = dev::mbar_wait_or(&op_free[slot], ((i / kOpRing) & 1) ^ 1, p.abort_flag);
+          if (w) dev::mbar_arrive(&op_done[slot]);
+        }
+        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
+      }
+    } else {
+      // completion warp: counts ops done group-wide and publishes flags, so
+      // the atomics / sys fences never stall the consumers' tile stream.
+      for (int i = 0; i < nops; ++i) {
+        const int opi = list[i];
+        const int slot = i % kOpRing;
+        bool w = true;
+        if (lane == 0) w = dev::mbar_wait_or(&op_done[slot], (i / kOpRing) & 1, p.abort_flag);
+        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
+        complete_op_warp(p, p.ops[opi], opi, gn);
+        if (lane == 0) dev::mbar_arrive(&op_free[slot]);
       }
     }
   } else {
@@ -472,6 +502,7 @@ struct themis_comm {
   uint64_t* trace = nullptr;
   bool trace_on = false;
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
+  int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -582,6 +613,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     return cuda_fail(e, "kernel attributes / occupancy query");
   }
   if (const char* env = getenv("THEMIS_COPY_ENGINE")) c->engine = std::string(env) == "ldg" ? 0 : 1;
+  if (const char* env = getenv("THEMIS_STAGES")) c->stages = std::max(1, std::min(kStages, atoi(env)));
   c->max_blocks = nb * c->num_sms;
   *out = c;
   return THEMIS_OK;
@@ -604,6 +636,11 @@ extern "C" themis_status_t themis_comm_status(themis_comm_t* c) {
 extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engine) {
   if (!c || engine < 0 || engine > 1) return fail(THEMIS_ERR_INVALID_ARG, "engine must be 0 (LDG) or 1 (TMA)");
   c->engine = engine;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_stages(themis_comm_t* c, int32_t stages) {
+  if (!c || stages < 1 || stages > kStages) return fail(THEMIS_ERR_INVALID_ARG, "stages must be 1..6");
+  c->stages = stages;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_pacing(themis_comm_t* c, int32_t on) {
@@ -795,6 +832,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.herr = c->herr_dev;
   kp.timeout_ns = c->timeout_ns;
   kp.trace = c->trace_on ? c->trace : nullptr;
+  kp.stages = c->stages;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;

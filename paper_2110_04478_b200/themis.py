@@ -229,6 +229,10 @@ class Comm:
         """Cap each dim at its topology bw_mbps by pacing (BW emulation)."""
         check(lib().themis_comm_set_pacing(self.h, int(on)))
 
+    def set_stages(self, stages: int) -> None:
+        """TMA ring depth per CTA (bytes in flight = stages x 32 KiB)."""
+        check(lib().themis_comm_set_stages(self.h, int(stages)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
 
