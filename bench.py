@@ -156,10 +156,23 @@ def run_themis(a):
     N = S // 4
     ratio = tuple(int(x) for x in a.ratio.split(":"))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    total_ctas = a.ctas_total or sms
+    # CTA budget / TMA ring depth (K5 calibration, profiles/r01_nvlink_calibration.md):
+    # NVLink saturates with ~4 MB in flight per GPU (32 CTAs x 4 x 32 KiB);
+    # more in-flight requests lose bandwidth.  HBM-resident dims want all SMs.
+    ncross_ = len(lay["cross_gpu_dims"])
+    if a.ctas_total:
+        total_ctas = a.ctas_total
+    elif ncross_ == 0:
+        total_ctas = sms
+    elif ncross_ == len(SIZES):
+        total_ctas = 32
+    else:
+        total_ctas = 96
+    stages = a.stages or (6 if ncross_ == 0 else 4)
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
     comm.set_timeout(30.0)
+    comm.set_stages(stages)
     pristine = [device_input(rank * V + v, N, "f32", dev) for v in range(V)]
 
     def refill():
@@ -323,7 +336,7 @@ def run_themis(a):
                        "topology": "x".join(map(str, SIZES)), "bytes_per_rank": S, "chunks": a.chunks,
                        "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
-                       "ctas_per_dim": main.bound_ctas(), "engine": "tma",
+                       "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
                        "aggregate_bus_gbs": round(busbw(t_main) * P, 1),
                        "best_step_bus_gbs": round(busbw(t_best), 2),
@@ -410,6 +423,7 @@ def main():
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
     ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")
     ap.add_argument("--compare-ratios", default="", help="extra emulated ratios, e.g. '1:1:1,2:2:1'")
     a = ap.parse_args()
