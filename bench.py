@@ -166,8 +166,8 @@ def run_themis(a):
         total_ctas = sms
     elif ncross_ == len(SIZES):
         total_ctas = 32
-    else:
-        total_ctas = 96
+    else:   # mixed: GPU-local dims (HBM) want many CTAs
+        total_ctas = sms if V >= 4 else 96
     stages = a.stages or (6 if ncross_ == 0 else 4)
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
@@ -221,7 +221,7 @@ def run_themis(a):
     # Paced budget per rank that this box can carry: NVLink (~700 GB/s per GPU
     # over the cross-GPU dims' share) and HBM (~6 TB/s at ~2.5 B per bus byte).
     ncross = len(lay["cross_gpu_dims"])
-    caps_ = [720.0, 6000.0 / (2.5 * V)]
+    caps_ = [560.0, 6000.0 / (2.5 * V)]   # 560 ~ 0.87 x the ~645 GB/s measured NVLink busBW
     if ncross:
         caps_.append(700.0 * len(SIZES) / (V * ncross))
     pace_gbs = a.pace_gbs or float(int(min(caps_) // 24) * 24)

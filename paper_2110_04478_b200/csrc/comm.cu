@@ -69,6 +69,7 @@ struct KParams {
   int32_t elem_size;
   uint32_t epoch;
   uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
+  unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
   uint32_t* done_cnt;
   uint32_t* abort_flag;     // device-local: someone timed out
   uint32_t* herr;           // host-mapped error word
@@ -230,7 +231,7 @@ __device__ __forceinline__ OpRange op_range(const KParams& p, const OpDesc& d, i
 }
 
 // Producer (one lane): stream the op's tiles into the shared-memory ring.
-__device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, const OpRange& r, char* smem,
+__device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, int opi, const OpRange& r, char* smem,
                                            uint64_t* full, uint64_t* empty, uint32_t& ctr) {
   const int k = d.dim;
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
@@ -238,7 +239,14 @@ __device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, co
   // faster than V * BW_k / c_k (the bound topology's bw, R6).  Due times are
   // absolute from the op start, so timer granularity does not accumulate.
   const float pace = p.pace_ns_per_byte[k];
-  const uint64_t t_op = pace > 0.f ? dev::globaltimer() : 0;
+  // The pacing origin is shared by the group's CTAs (first starter wins), so
+  // a CTA that starts an op late catches up instead of stretching the op.
+  uint64_t t_op = 0;
+  if (pace > 0.f) {
+    const unsigned long long now = dev::globaltimer();
+    const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
+    t_op = prev ? prev : now;
+  }
   double sent = 0.0;
   for (uint64_t it = r.u0 / r.Lb; it * r.Lb < r.u1; ++it) {
     const Item m = decode_item(p, d, it);
@@ -326,6 +334,7 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
     last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
     if (last) {
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
+      p.op_t0[opi] = 0;
       dev::fence_acq_rel_sys();
     }
   }
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         if (d.stage > 0 && !wait_deps_warp(p, d, opi)) break;
         if (lane == 0) {
           if (p.trace && gi == 0) p.trace[2 * opi] = dev::globaltimer();
-          produce_op(p, d, r, smem, full, empty, ctr);
+          produce_op(p, d, opi, r, smem, full, empty, ctr);
         }
         __syncwarp();
       }
@@ -495,6 +504,7 @@ struct themis_comm {
   uint64_t heap_bytes = 0, vrank_stride = 0, sig_bytes = 0;
   uint32_t epoch = 0;
   uint32_t* opcnt = nullptr;
+  unsigned long long* op_t0 = nullptr;
   uint32_t* done_cnt = nullptr;
   uint32_t* abort_flag = nullptr;
   uint32_t* herr_host = nullptr;
@@ -594,6 +604,8 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
       (e = cudaMalloc(&c->opcnt, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
+      (e = cudaMalloc(&c->op_t0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
+      (e = cudaMemset(c->op_t0, 0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->opcnt, 0, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
       (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 2 * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 2 * kMaxOps)) != cudaSuccess ||
@@ -622,6 +634,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
 extern "C" void themis_comm_free(themis_comm_t* c) {
   if (!c) return;
   cudaFree(c->opcnt);
+  cudaFree(c->op_t0);
   cudaFree(c->trace);
   cudaFreeHost(c->herr_host);
   delete c;
@@ -827,6 +840,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.elem_size = esz;
   kp.epoch = ++c->epoch;
   kp.opcnt = c->opcnt;
+  kp.op_t0 = c->op_t0;
   kp.done_cnt = c->done_cnt;
   kp.abort_flag = c->abort_flag;
   kp.herr = c->herr_dev;
