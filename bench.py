@@ -221,9 +221,11 @@ def run_themis(a):
     # Paced budget per rank that this box can carry: NVLink (~700 GB/s per GPU
     # over the cross-GPU dims' share) and HBM (~6 TB/s at ~2.5 B per bus byte).
     ncross = len(lay["cross_gpu_dims"])
-    caps_ = [560.0, 6000.0 / (2.5 * V)]   # 560 ~ 0.87 x the ~645 GB/s measured NVLink busBW
+    # ~80% of the physical limits, so the emulated BW (not the fabric) binds
+    # even when Themis keeps every dimension busy at once.
+    caps_ = [500.0, 0.8 * 6000.0 / (2.5 * V)]
     if ncross:
-        caps_.append(700.0 * len(SIZES) / (V * ncross))
+        caps_.append(500.0 * len(SIZES) / (V * ncross))
     pace_gbs = a.pace_gbs or float(int(min(caps_) // 24) * 24)
     if not a.no_compare:
         for mode in ("caps", "paced"):

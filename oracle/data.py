@@ -110,17 +110,29 @@ def _groups(topo, k):
     return [topo.dim_peers(r, k) for r in range(topo.P) if topo.coords(r)[k] == 0]
 
 
+def summation_order(topo, k, t) -> list:
+    """Member order in which part t (digit_k = t) is summed on dim k.
+    Direct / switch dims: coordinate order 0..P_k-1 (R18).  Ring dims
+    (Table 1; figure RingAllReduce :214): the partial travels the
+    ring and ends at its owner t, so it is x_{t+1} + x_{t+2} + ... + x_t."""
+    pk = topo.dims[k].size
+    if topo.dims[k].kind == "ring" and pk >= 3:
+        return [(t + 1 + i) % pk for i in range(pk)]
+    return list(range(pk))
+
+
 def apply_rs(bufs, topo, C, c, k, reduced, dtype):
     N = bufs[0].shape[0]
     for members in _groups(topo, k):
         new = []
         for t, mt in enumerate(members):
             ct = topo.coords(mt)
+            order = summation_order(topo, k, t)
             for b in held_blocks(topo, ct, reduced):
                 if digit(topo, b, k) != t:
                     continue
                 s = slice_of(N, topo.P, C, c, b)
-                new.append((mt, s, reduce_in_order([bufs[mj][s] for mj in members], dtype)))
+                new.append((mt, s, reduce_in_order([bufs[members[j]][s] for j in order], dtype)))
         for mt, s, v in new:
             bufs[mt][s] = v
 

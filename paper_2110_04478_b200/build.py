@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libthemis.so")
 SOURCES = ["planner.cpp", "comm.cu"]
-HEADERS = ["plan_internal.h", "device.cuh"]
+HEADERS = ["plan_internal.h", "device.cuh", "exec_kernel.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

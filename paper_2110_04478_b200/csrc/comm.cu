@@ -31,7 +31,6 @@ constexpr int kMaxOps = THEMIS_MAX_CHUNKS * 2 * THEMIS_MAX_DIMS;    // ops per p
 constexpr uint64_t kAlign = 1ull << 16;
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
-uint64_t signal_bytes(int P) { return round_up(4ull * (2ull * P + (uint64_t)P * kMaxOps), kAlign); }
 
 themis_status_t cuda_fail(cudaError_t e, const char* what) {
   return fail(THEMIS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -42,441 +41,9 @@ themis_status_t cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, #call); \
   } while (0)
 
-// Per-op descriptor uploaded at bind (a5).
-struct OpDesc {
-  int32_t chunk, stage, dim, phase;  // phase 0 RS, 1 AG
-  uint32_t reduced;                  // dims reduce-scattered before the op
-  int32_t next_dim;                  // dim of stage+1 (-1: last stage)
-  int32_t nfree;                     // dims whose block digit is free
-  int32_t free_size[THEMIS_MAX_DIMS];
-  int64_t free_stride[THEMIS_MAX_DIMS];
-  int64_t nblk;                      // prod free sizes
-};
+#include "exec_kernel.cuh"
 
-struct KParams {
-  int32_t D, P, V, W, my_gpu, C, NS;
-  int32_t size[THEMIS_MAX_DIMS];
-  int64_t stride[THEMIS_MAX_DIMS];
-  int32_t grp_start[THEMIS_MAX_DIMS + 1];
-  int32_t dim_ops_n[THEMIS_MAX_DIMS];
-  const OpDesc* ops;        // [C*NS]
-  const int32_t* dim_ops;   // [D][C*NS] op indices c*NS+s
-  char* heap[THEMIS_MAX_GPUS];
-  uint64_t data_rel;        // buf - heap[my_gpu]
-  uint64_t vrank_stride, sig_bytes;
-  uint64_t blk_elems;       // N / P
-  uint64_t slice_elems;     // N / (P*C)
-  int32_t elem_size;
-  uint32_t epoch;
-  uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
-  unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
-  uint32_t* done_cnt;
-  uint32_t* abort_flag;     // device-local: someone timed out
-  uint32_t* herr;           // host-mapped error word
-  uint64_t timeout_ns;
-  uint64_t* trace;          // [C*NS*2] or null
-  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
-  int32_t stages;           // TMA ring depth in use (<= kStages): bytes in flight per CTA
-};
-
-__device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
-  return reinterpret_cast<uint32_t*>(p.heap[q / p.V] + (uint64_t)(q % p.V) * p.sig_bytes);
-}
-__device__ __forceinline__ uint32_t* entry_slot(const KParams& p, int q, int src) { return sig_of(p, q) + src; }
-__device__ __forceinline__ uint32_t* exit_slot(const KParams& p, int q, int src) { return sig_of(p, q) + p.P + src; }
-__device__ __forceinline__ uint32_t* ready_slot(const KParams& p, int q, int src, int op) {
-  return sig_of(p, q) + 2 * p.P + (uint64_t)src * kMaxOps + op;
-}
-__device__ __forceinline__ char* data_of(const KParams& p, int q) {
-  return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
-}
-__device__ __forceinline__ int coord(const KParams& p, int q, int k) { return (int)((q / p.stride[k]) % p.size[k]); }
-
-// Spin until *f >= e.  Returns false on timeout / abort (watchdog).
-__device__ bool wait_geq(const KParams& p, const uint32_t* f, uint32_t e, uint32_t where) {
-  if (dev::ld_acquire_sys(f) >= e) return true;
-  const uint64_t t0 = dev::globaltimer();
-  for (;;) {
-#pragma unroll 1
-    for (int i = 0; i < 256; ++i)
-      if (dev::ld_acquire_sys(f) >= e) return true;
-    if (*(volatile uint32_t*)p.abort_flag) return false;
-    if (dev::globaltimer() - t0 > p.timeout_ns) {
-      atomicExch(p.abort_flag, 1u);
-      *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_TIMEOUT | (where << 8);
-      __threadfence_system();
-      return false;
-    }
-  }
-}
-
-// ---------------------------------------------------------------- work items
-// An op's work on this GPU is a list of "items", each one contiguous slice
-// (chunk c of block b) of slice_bytes:
-//   RS: item = (local rank v, free index f)          -> V * nblk items
-//   AG: item = (local rank v, source member j != c_k, f) -> V * (P_k-1) * nblk
-// The op's total bytes are split evenly (16-byte granules) over the group's
-// CTAs; each CTA walks its contiguous range.
-struct Item {
-  int q;          // global logical rank this item belongs to
-  int g0;         // rank of member 0 of q's dim-k group
-  int j;          // AG: source member; RS: unused
-  uint64_t off;   // byte offset of the slice inside a rank's data region
-};
-
-__device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, uint64_t it) {
-  Item r;
-  const int k = d.dim, pk = p.size[k];
-  int64_t f;
-  int64_t b = 0;
-  if (d.phase == 0) {
-    r.q = p.my_gpu * p.V + (int)(it / d.nblk);
-    f = (int64_t)(it % d.nblk);
-    r.j = -1;
-    for (int dd = 0; dd < p.D; ++dd)  // fixed digits: my coords on reduced U {k}
-      if ((d.reduced >> dd & 1u) || dd == k) b += (int64_t)coord(p, r.q, dd) * p.stride[dd];
-  } else {
-    const uint64_t per_v = (uint64_t)(pk - 1) * d.nblk;
-    r.q = p.my_gpu * p.V + (int)(it / per_v);
-    const uint64_t rem = it % per_v;
-    const int jj = (int)(rem / d.nblk);
-    const int ck = coord(p, r.q, k);
-    r.j = jj < ck ? jj : jj + 1;
-    f = (int64_t)(rem % d.nblk);
-    b = (int64_t)r.j * p.stride[k];
-    for (int dd = 0; dd < p.D; ++dd)  // fixed digits: my coords on reduced \ {k}, digit_k = j
-      if ((d.reduced >> dd & 1u) && dd != k) b += (int64_t)coord(p, r.q, dd) * p.stride[dd];
-  }
-  for (int i = 0; i < d.nfree; ++i) {
-    b += (f % d.free_size[i]) * d.free_stride[i];
-    f /= d.free_size[i];
-  }
-  r.g0 = r.q - coord(p, r.q, k) * (int)p.stride[k];
-  r.off = ((uint64_t)b * p.blk_elems + (uint64_t)d.chunk * p.slice_elems) * p.elem_size;
-  return r;
-}
-
-__device__ __forceinline__ uint64_t op_items(const KParams& p, const OpDesc& d) {
-  const int pk = p.size[d.dim];
-  return (uint64_t)p.V * d.nblk * (d.phase == 0 ? 1 : (uint64_t)(pk - 1));
-}
-
-// Address of dim-k member j's copy of the current piece.
-struct PeerSrc {
-  const KParams* p;
-  int q0, step;
-  uint64_t off;
-  __device__ __forceinline__ const uint4* operator()(int j) const {
-    return reinterpret_cast<const uint4*>(data_of(*p, q0 + j * step) + off);
-  }
-};
-
-// ------------------------------------------------------- path 1: LDG / STG
-// Every thread issues NSRC*UNROLL 16-byte L1-bypassing loads before adding.
-template <class Tag>
-__device__ void run_op_ldg(const KParams& p, const OpDesc& d, int gi, int gn) {
-  const int k = d.dim, pk = p.size[k];
-  const uint64_t Lv = p.slice_elems * p.elem_size / 16;
-  const uint64_t total = op_items(p, d) * Lv;
-  const uint64_t u0 = total * gi / gn, u1 = total * (gi + 1) / gn;
-  for (uint64_t it = u0 / Lv; it * Lv < u1; ++it) {
-    const Item m = decode_item(p, d, it);
-    const uint64_t a = (u0 > it * Lv ? u0 - it * Lv : 0);
-    const uint64_t e = (u1 - it * Lv < Lv ? u1 - it * Lv : Lv);
-    uint4* dst = reinterpret_cast<uint4*>(data_of(p, m.q) + m.off);
-    const PeerSrc src{&p, m.g0, (int)p.stride[k], m.off};
-    if (d.phase == 1) {
-      dev::copy_range<8>(dst, src(m.j), a, e);
-      continue;
-    }
-    switch (pk) {
-      case 2: dev::reduce_range<Tag, 2, 4>(dst, src, a, e); break;
-      case 3: dev::reduce_range<Tag, 3, 4>(dst, src, a, e); break;
-      case 4: dev::reduce_range<Tag, 4, 2>(dst, src, a, e); break;
-      case 8: dev::reduce_range<Tag, 8, 1>(dst, src, a, e); break;
-      default: dev::reduce_range_generic<Tag>(dst, src, pk, a, e); break;
-    }
-  }
-}
-
-// ------------------------------------------------------- path 2: TMA bulk
-// Warp 0 lane 0 streams each tile's P_k (RS) or 1 (AG) source ranges into a
-// kStages-deep shared-memory ring with cp.async.bulk (mbarrier complete_tx);
-// the kConsumerWarps consumer warps sum the P_k copies in coordinate order
-// (RS) or pass the bytes through (AG) and store with 16-byte STG.
-constexpr int kStages = 6;
-constexpr int kStageBytes = 32 * 1024;
-constexpr int kConsumerWarps = 8;
-constexpr int kOpRing = 16;  // ops the consumers may run ahead of the completion warp
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * (kStages + kOpRing) * 8;
-static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + completion warp");
-
-// Geometry of op d for CTA gi of gn: byte range [u0, u1) of the op's items
-// (16-byte granules), TMA tile size per source.
-struct OpRange {
-  uint64_t u0, u1, Lb;
-  uint32_t tile;
-  int nsrc, pk;
-};
-__device__ __forceinline__ OpRange op_range(const KParams& p, const OpDesc& d, int gi, int gn) {
-  OpRange r;
-  r.pk = p.size[d.dim];
-  r.nsrc = d.phase == 0 ? r.pk : 1;
-  r.Lb = p.slice_elems * p.elem_size;
-  const uint64_t tot16 = op_items(p, d) * (r.Lb / 16);
-  r.u0 = tot16 * gi / gn * 16;
-  r.u1 = tot16 * (gi + 1) / gn * 16;
-  r.tile = ((uint32_t)kStageBytes / r.nsrc) & ~15u;
-  return r;
-}
-
-// Producer (one lane): stream the op's tiles into the shared-memory ring.
-__device__ __forceinline__ void produce_op(const KParams& p, const OpDesc& d, int opi, const OpRange& r, char* smem,
-                                           uint64_t* full, uint64_t* empty, uint32_t& ctr) {
-  const int k = d.dim;
-  dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
-  // Bandwidth emulation by pacing: this CTA pulls peer bytes of this op no
-  // faster than V * BW_k / c_k (the bound topology's bw, R6).  Due times are
-  // absolute from the op start, so timer granularity does not accumulate.
-  const float pace = p.pace_ns_per_byte[k];
-  // The pacing origin is shared by the group's CTAs (first starter wins), so
-  // a CTA that starts an op late catches up instead of stretching the op.
-  uint64_t t_op = 0;
-  if (pace > 0.f) {
-    const unsigned long long now = dev::globaltimer();
-    const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
-    t_op = prev ? prev : now;
-  }
-  double sent = 0.0;
-  for (uint64_t it = r.u0 / r.Lb; it * r.Lb < r.u1; ++it) {
-    const Item m = decode_item(p, d, it);
-    const uint64_t a = (r.u0 > it * r.Lb ? r.u0 - it * r.Lb : 0);
-    const uint64_t e = (r.u1 - it * r.Lb < r.Lb ? r.u1 - it * r.Lb : r.Lb);
-    for (uint64_t pos = a; pos < e; pos += r.tile, ++ctr) {
-      const uint32_t bytes = (uint32_t)(e - pos < r.tile ? e - pos : r.tile);
-      if (pace > 0.f) {
-        const uint64_t due = t_op + (uint64_t)(sent * pace);
-        while (dev::globaltimer() < due) {
-        }
-        sent += (double)bytes * (d.phase == 0 ? r.pk - 1 : 1);
-      }
-      const int s = ctr % p.stages;
-      dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
-      dev::mbar_expect_tx(&full[s], bytes * r.nsrc);
-      char* dst = smem + s * kStageBytes;
-      if (d.phase == 0) {
-        for (int j = 0; j < r.pk; ++j)
-          dev::bulk_g2s(dst + j * r.tile, data_of(p, m.g0 + j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
-      } else {
-        dev::bulk_g2s(dst, data_of(p, m.g0 + m.j * (int)p.stride[k]) + m.off + pos, bytes, &full[s]);
-      }
-    }
-  }
-}
-
-// Consumers (warps 1..kConsumerWarps): sum the P_k copies of each tile in
-// coordinate order (RS) or pass the bytes through (AG), 16-byte STG.
-// Returns false if the kernel is aborting (watchdog).
-template <class Tag>
-__device__ __forceinline__ bool consume_op(const KParams& p, const OpDesc& d, const OpRange& r, const char* smem,
-                                           uint64_t* full, uint64_t* empty, uint32_t& ctr) {
-  const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
-  constexpr int kCons = 32 * kConsumerWarps;
-  const uint32_t tile16 = r.tile / 16;
-  for (uint64_t it = r.u0 / r.Lb; it * r.Lb < r.u1; ++it) {
-    const Item m = decode_item(p, d, it);
-    const uint64_t a = (r.u0 > it * r.Lb ? r.u0 - it * r.Lb : 0);
-    const uint64_t e = (r.u1 - it * r.Lb < r.Lb ? r.u1 - it * r.Lb : r.Lb);
-    char* base = data_of(p, m.q) + m.off;
-    for (uint64_t pos = a; pos < e; pos += r.tile, ++ctr) {
-      const uint32_t n16 = (uint32_t)((e - pos < r.tile ? e - pos : r.tile) / 16);
-      const int s = ctr % p.stages;
-      if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
-      const uint4* sm = reinterpret_cast<const uint4*>(smem + s * kStageBytes);
-      uint4* dst = reinterpret_cast<uint4*>(base + pos);
-      if (d.phase == 0) {
-        for (uint32_t w = ct; w < n16; w += kCons) {
-          float acc[Tag::kAcc];
-          Tag::load(acc, sm[w]);
-          for (int j = 1; j < r.pk; ++j) Tag::add(acc, sm[j * tile16 + w]);
-          dev::st_v4(dst + w, Tag::store(acc));
-        }
-      } else {
-        for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
-      }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
-    }
-  }
-  return true;
-}
-
-// One warp: wait until the local ranks and their dim-k peers completed (c, s-1).
-__device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d, int opi) {
-  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
-  bool ok = true;
-  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
-    const int q = q0 + t / pk;
-    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
-  }
-  return __all_sync(0xFFFFFFFFu, ok);
-}
-
-// One warp: count this CTA's completion of op opi; the group's last CTA
-// publishes the epoch to the consumers of (c, s): self and the next stage's
-// dim peers.  Release chain: consumers' stores -> named barrier ->
-// atom.acq_rel.gpu (all CTAs) -> fence.acq_rel.sys -> relaxed sys stores.
-__device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc& d, int opi, int gn) {
-  const int lane = threadIdx.x & 31;
-  uint32_t last = 0;
-  if (lane == 0) {
-    last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
-    if (last) {
-      p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
-      p.op_t0[opi] = 0;
-      dev::fence_acq_rel_sys();
-    }
-  }
-  last = __shfl_sync(0xFFFFFFFFu, last, 0);
-  if (!last) return;
-  if (d.next_dim >= 0) {
-    const int V = p.V, q0 = p.my_gpu * V, kn = d.next_dim, pn = p.size[kn];
-    for (int t = lane; t < V * pn; t += 32) {
-      const int q = q0 + t / pn;
-      const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
-      dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
-    }
-  }
-  if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
-  __syncwarp();
-}
-
-template <class Tag, bool kTma>
-__global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_constant__ KParams p) {
-  extern __shared__ __align__(128) char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* op_done = empty + kStages;
-  uint64_t* op_free = op_done + kOpRing;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  int g = 0;
-  while (g + 1 < p.D && (int)blockIdx.x >= p.grp_start[g + 1]) ++g;
-  const int gi = blockIdx.x - p.grp_start[g];
-  const int gn = p.grp_start[g + 1] - p.grp_start[g];
-  const int V = p.V, P = p.P;
-  const int q0 = p.my_gpu * V;
-  bool ok = true;
-  if (kTma && tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], kConsumerWarps);
-    }
-    for (int s = 0; s < kOpRing; ++s) {
-      dev::mbar_init(&op_done[s], kConsumerWarps);
-      dev::mbar_init(&op_free[s], 1);
-    }
-    dev::fence_mbar_init();
-  }
-
-  // a6: entry barrier — every local rank announces the epoch to every rank.
-  if (blockIdx.x == 0)
-    for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), p.epoch);
-  for (int i = tid; i < V * P; i += blockDim.x)
-    ok &= wait_geq(p, entry_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFFu);
-  ok = __syncthreads_and(ok);
-
-  // a9: walk this dimension's ops in the enforced order.
-  const int* list = p.dim_ops + (uint64_t)g * p.C * p.NS;
-  const int nops = ok ? p.dim_ops_n[g] : 0;
-  if constexpr (kTma) {
-    // Warp-specialised and decoupled: the producer warp waits for an op's
-    // dependencies and streams its tiles, then moves on to the next op while
-    // the consumer warps finish; the consumers count and publish completion.
-    uint32_t ctr = 0;  // ring position (identical sequence in producer and consumers)
-    if (warp == 0) {
-      for (int i = 0; i < nops; ++i) {
-        const int opi = list[i];
-        const OpDesc& d = p.ops[opi];
-        const OpRange r = op_range(p, d, gi, gn);
-        if (r.u0 >= r.u1) continue;  // no bytes for this CTA: nothing to wait for
-        if (d.stage > 0 && !wait_deps_warp(p, d, opi)) break;
-        if (lane == 0) {
-          if (p.trace && gi == 0) p.trace[2 * opi] = dev::globaltimer();
-          produce_op(p, d, opi, r, smem, full, empty, ctr);
-        }
-        __syncwarp();
-      }
-    } else if (warp <= kConsumerWarps) {
-      // consumers: per op, every consumer warp arrives on op_done[slot]
-      // (mbarrier arrive = release.cta of its stores) once it is done, after
-      // the completion warp has freed that slot (ring of kOpRing ops).
-      for (int i = 0; i < nops; ++i) {
-        const int opi = list[i];
-        const OpDesc& d = p.ops[opi];
-        const OpRange r = op_range(p, d, gi, gn);
-        if (!consume_op<Tag>(p, d, r, smem, full, empty, ctr)) break;
-        __syncwarp();
-        bool w = true;
-        if (lane == 0) {
-          const int slot = i % kOpRing;
-          w = dev::mbar_wait_or(&op_free[slot], ((i / kOpRing) & 1) ^ 1, p.abort_flag);
-          if (w) dev::mbar_arrive(&op_done[slot]);
-        }
-        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
-      }
-    } else {
-      // completion warp: counts ops done group-wide and publishes flags, so
-      // the atomics / sys fences never stall the consumers' tile stream.
-      for (int i = 0; i < nops; ++i) {
-        const int opi = list[i];
-        const int slot = i % kOpRing;
-        bool w = true;
-        if (lane == 0) w = dev::mbar_wait_or(&op_done[slot], (i / kOpRing) & 1, p.abort_flag);
-        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
-        complete_op_warp(p, p.ops[opi], opi, gn);
-        if (lane == 0) dev::mbar_arrive(&op_free[slot]);
-      }
-    }
-  } else {
-    for (int i = 0; ok && i < nops; ++i) {
-      const int opi = list[i];
-      const OpDesc& d = p.ops[opi];
-      const int k = d.dim;
-      if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
-        const int pk = p.size[k];
-        for (int t = tid; t < V * pk; t += blockDim.x) {
-          const int q = q0 + t / pk;
-          const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
-        }
-        ok = __syncthreads_and(ok);
-        if (!ok) break;
-      }
-      if (p.trace && gi == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
-      run_op_ldg<Tag>(p, d, gi, gn);
-      __syncthreads();
-      if (warp == 0) complete_op_warp(p, d, opi, gn);
-      __syncthreads();
-    }
-  }
-
-  // exit: all CTAs done -> exit barrier so no peer still reads our buffers.
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence_system();
-    atomicAdd(p.done_cnt, 1u);
-  }
-  if (blockIdx.x != 0) return;
-  if (tid == 0) {
-    ok &= wait_geq(p, p.done_cnt, gridDim.x, 0xFFFFFEu);
-    *p.done_cnt = 0;
-    __threadfence_system();
-  }
-  __syncthreads();
-  for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(exit_slot(p, i % P, q0 + i / P), p.epoch);
-  for (int i = tid; i < V * P; i += blockDim.x) wait_geq(p, exit_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFDu);
-}
+uint64_t signal_bytes(int P) { return round_up(pad_bytes(P), kAlign); }
 
 }  // namespace
 
@@ -751,14 +318,20 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
       }
       stride *= pl->topo.size[k];
     }
+    // Table 1: ring dims run the ring algorithm (P_k = 2 ring == direct)
+    d.ring = pl->topo.kind[o.dim] == THEMIS_DIM_RING && pl->topo.size[o.dim] >= 3;
     ops[i] = d;
   }
   std::vector<int32_t> lists((size_t)D * pl->C * pl->NS, 0);
   for (int k = 0; k < D; ++k)
     for (size_t i = 0; i < pl->dim_ops[k].size(); ++i) {
       uint32_t e = pl->dim_ops[k][i];
-      lists[(size_t)k * pl->C * pl->NS + i] = (int32_t)((e >> 8) * pl->NS + (e & 0xFF));
+      const int opi = (int)((e >> 8) * pl->NS + (e & 0xFF));
+      lists[(size_t)k * pl->C * pl->NS + i] = opi;
+      ops[opi].seq = (int32_t)i;
     }
+  for (int k = 0; k < D; ++k)
+    if (n[k] > kMaxCtas) return fail(THEMIS_ERR_INVALID_ARG, "at most 160 CTAs per dimension group");
   free_bind(pl);
   auto* b = new BindState();
   b->comm = c;
@@ -852,6 +425,10 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
 
   void* args[] = {&kp};
+  if (!c->engine)
+    for (int k = 0; k < pl->D; ++k)
+      if (pl->topo.kind[k] == THEMIS_DIM_RING && pl->topo.size[k] >= 3)
+        return fail(THEMIS_ERR_INVALID_ARG, "ring dimensions need the TMA engine (themis_comm_set_engine(comm, 1))");
   const void* fn = kernel_for(dtype, c->engine);
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(pl->bind->total_ctas), dim3(kThreads), args,
                                               c->engine ? kSmemBytes : 0,

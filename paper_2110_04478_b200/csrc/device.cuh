@@ -279,3 +279,16 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 }  // namespace dev
 }  // namespace themis
+
+namespace themis {
+namespace dev {
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+}  // namespace dev
+}  // namespace themis

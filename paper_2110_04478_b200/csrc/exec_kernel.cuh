@@ -1,0 +1,594 @@
+// exec_kernel.cuh — device side of the Themis executor (included by comm.cu
+// inside its anonymous namespace, after the shared constants).
+//
+// One cooperative launch per collective; CTAs are partitioned into D
+// "dimension groups"; group k walks the plan's op list for dim k in the
+// enforced order.  Each op (chunk c, stage s, dim k) is one
+// stage of the hierarchical collective for every local logical rank and is
+// executed with the basic algorithm Table 1 assigns to the dimension
+// (PAPER.md:226-238):
+//   direct (FullyConnected; also used for Switch dims):
+//     RS: y = x_0 + x_1 + ... + x_{P_k-1} over the kept part (digit_k = c_k),
+//         one pull of every member's copy, summed in coordinate order (R18);
+//     AG: copy every member j's held part (digit_k = j).
+//   ring (P_k >= 3): P_k - 1 neighbour steps (PAPER.md:214 figure
+//     RingAllReduce, :477).  RS step i: part p = (c_k + P_k - 2 - i) mod P_k,
+//     partial = left's partial (left's original at i = 0) + own value; after
+//     the last step the rank holds its own part (digit_k = c_k) fully reduced.
+//     AG step i: copy part (c_k - 1 - i) mod P_k from the left neighbour.
+// A "unit" is one direct op or one ring step.
+
+constexpr int kMaxCtas = 160;  // CTAs per dimension group (ring step flags)
+enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3 };
+
+// Per-op descriptor uploaded at bind (a5).
+struct OpDesc {
+  int32_t chunk, stage, dim, phase;  // phase 0 RS, 1 AG
+  uint32_t reduced;                  // dims reduce-scattered before the op
+  int32_t next_dim;                  // dim of stage+1 (-1: last stage)
+  int32_t ring;                      // 1: ring algorithm on this dim
+  int32_t seq;                       // index of the op in its dim's enforced list
+  int32_t nfree;                     // dims whose block digit is free
+  int32_t free_size[THEMIS_MAX_DIMS];
+  int64_t free_stride[THEMIS_MAX_DIMS];
+  int64_t nblk;                      // prod free sizes
+};
+
+struct KParams {
+  int32_t D, P, V, W, my_gpu, C, NS;
+  int32_t size[THEMIS_MAX_DIMS];
+  int64_t stride[THEMIS_MAX_DIMS];
+  int32_t grp_start[THEMIS_MAX_DIMS + 1];
+  int32_t dim_ops_n[THEMIS_MAX_DIMS];
+  const OpDesc* ops;        // [C*NS]
+  const int32_t* dim_ops;   // [D][C*NS] op indices c*NS+s
+  char* heap[THEMIS_MAX_GPUS];
+  uint64_t data_rel;        // buf - heap[my_gpu]
+  uint64_t vrank_stride, sig_bytes;
+  uint64_t blk_elems;       // N / P
+  uint64_t slice_elems;     // N / (P*C)
+  int32_t elem_size;
+  uint32_t epoch;
+  uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
+  unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
+  uint32_t* done_cnt;
+  uint32_t* abort_flag;     // device-local: someone timed out
+  uint32_t* herr;           // host-mapped error word
+  uint64_t timeout_ns;
+  uint64_t* trace;          // [C*NS*2] or null
+  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
+  int32_t stages;           // TMA ring depth in use (<= kStages): bytes in flight per CTA
+};
+
+// ---------------------------------------------------------------- signal pads
+// pad(q) = [entry u32 P][exit u32 P][ready u32 P x kMaxOps][ring u64 P x 8 x kMaxCtas]
+__host__ __device__ __forceinline__ uint64_t ring_flags_offset(int P) { return 4ull * (2ull * P + (uint64_t)P * kMaxOps); }
+__host__ __device__ __forceinline__ uint64_t pad_bytes(int P) {
+  return ring_flags_offset(P) + 8ull * P * THEMIS_MAX_DIMS * kMaxCtas;
+}
+__device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
+  return reinterpret_cast<uint32_t*>(p.heap[q / p.V] + (uint64_t)(q % p.V) * p.sig_bytes);
+}
+__device__ __forceinline__ uint32_t* entry_slot(const KParams& p, int q, int src) { return sig_of(p, q) + src; }
+__device__ __forceinline__ uint32_t* exit_slot(const KParams& p, int q, int src) { return sig_of(p, q) + p.P + src; }
+__device__ __forceinline__ uint32_t* ready_slot(const KParams& p, int q, int src, int op) {
+  return sig_of(p, q) + 2 * p.P + (uint64_t)src * kMaxOps + op;
+}
+// ring step flag written by rank `src`'s CTA g of dim k's group into q's pad
+__device__ __forceinline__ unsigned long long* ring_slot(const KParams& p, int q, int src, int k, int g) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig_of(p, q)) + ring_flags_offset(p.P)) +
+         ((uint64_t)src * THEMIS_MAX_DIMS + k) * kMaxCtas + g;
+}
+__device__ __forceinline__ char* data_of(const KParams& p, int q) {
+  return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
+}
+__device__ __forceinline__ int coord(const KParams& p, int q, int k) { return (int)((q / p.stride[k]) % p.size[k]); }
+// neighbour of q on dim k at coordinate offset delta (ring left = -1, right = +1)
+__device__ __forceinline__ int ring_peer(const KParams& p, int q, int k, int delta) {
+  const int pk = p.size[k], c = coord(p, q, k);
+  return q + (((c + delta) % pk + pk) % pk - c) * (int)p.stride[k];
+}
+
+// Spin until *f >= e.  Returns false on timeout / abort (watchdog).
+__device__ bool wait_geq(const KParams& p, const uint32_t* f, uint32_t e, uint32_t where) {
+  if (dev::ld_acquire_sys(f) >= e) return true;
+  const uint64_t t0 = dev::globaltimer();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 256; ++i)
+      if (dev::ld_acquire_sys(f) >= e) return true;
+    if (*(volatile uint32_t*)p.abort_flag) return false;
+    if (dev::globaltimer() - t0 > p.timeout_ns) {
+      atomicExch(p.abort_flag, 1u);
+      *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_TIMEOUT | (where << 8);
+      __threadfence_system();
+      return false;
+    }
+  }
+}
+__device__ bool wait_geq64(const KParams& p, const unsigned long long* f, unsigned long long e, uint32_t where) {
+  if (dev::ld_acquire_sys64(f) >= e) return true;
+  const uint64_t t0 = dev::globaltimer();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 256; ++i)
+      if (dev::ld_acquire_sys64(f) >= e) return true;
+    if (*(volatile uint32_t*)p.abort_flag) return false;
+    if (dev::globaltimer() - t0 > p.timeout_ns) {
+      atomicExch(p.abort_flag, 1u);
+      *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_TIMEOUT | (where << 8);
+      __threadfence_system();
+      return false;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- work items
+// An item is one contiguous slice (chunk c of block b, slice_bytes) of one
+// local rank:  direct RS / ring RS / ring AG: (local rank v, free index f) ->
+// V * nblk items;  direct AG: (v, source member j != c_k, f) -> V*(P_k-1)*nblk.
+struct Item {
+  int q;          // global logical rank the item belongs to
+  int g0;         // rank of member 0 of q's dim-k group
+  int j;          // direct AG: source member
+  uint64_t off;   // byte offset of the slice inside a rank's data region
+};
+
+__device__ __forceinline__ int unit_mode(const OpDesc& d) {
+  return d.ring ? (d.phase == 0 ? U_RING_RS : U_RING_AG) : (d.phase == 0 ? U_DIRECT_RS : U_DIRECT_AG);
+}
+__device__ __forceinline__ uint64_t unit_items(const KParams& p, const OpDesc& d, int mode) {
+  return (uint64_t)p.V * d.nblk * (mode == U_DIRECT_AG ? (uint64_t)(p.size[d.dim] - 1) : 1ull);
+}
+
+__device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, int mode, int step, uint64_t it) {
+  Item r;
+  const int k = d.dim, pk = p.size[k];
+  int64_t f;
+  int digit;
+  if (mode == U_DIRECT_AG) {
+    const uint64_t per_v = (uint64_t)(pk - 1) * d.nblk;
+    r.q = p.my_gpu * p.V + (int)(it / per_v);
+    const uint64_t rem = it % per_v;
+    const int jj = (int)(rem / d.nblk);
+    const int ck = coord(p, r.q, k);
+    r.j = jj < ck ? jj : jj + 1;
+    f = (int64_t)(rem % d.nblk);
+    digit = r.j;
+  } else {
+    r.q = p.my_gpu * p.V + (int)(it / d.nblk);
+    f = (int64_t)(it % d.nblk);
+    r.j = -1;
+    const int ck = coord(p, r.q, k);
+    digit = mode == U_DIRECT_RS ? ck
+          : mode == U_RING_RS   ? (ck + pk - 2 - step) % pk
+                                : ((ck - 1 - step) % pk + pk) % pk;
+  }
+  int64_t b = (int64_t)digit * p.stride[k];
+  for (int dd = 0; dd < p.D; ++dd)  // other fixed digits: the rank's coords on the reduced dims
+    if ((d.reduced >> dd & 1u) && dd != k) b += (int64_t)coord(p, r.q, dd) * p.stride[dd];
+  for (int i = 0; i < d.nfree; ++i) {
+    b += (f % d.free_size[i]) * d.free_stride[i];
+    f /= d.free_size[i];
+  }
+  r.g0 = r.q - coord(p, r.q, k) * (int)p.stride[k];
+  r.off = ((uint64_t)b * p.blk_elems + (uint64_t)d.chunk * p.slice_elems) * p.elem_size;
+  return r;
+}
+
+// Visit this CTA's byte spans of a unit: fn(item index, a, e) with [a, e)
+// inside the item.  Direct units split the unit's bytes evenly over the group;
+// ring units give CTA g the same sub-range of every rank's part, so a ring
+// step depends only on CTA g of the left neighbour.
+template <class F>
+__device__ __forceinline__ void for_each_span(const KParams& p, const OpDesc& d, int mode, int gi, int gn, F&& fn) {
+  const uint64_t Lb = p.slice_elems * p.elem_size;
+  if (mode == U_RING_RS || mode == U_RING_AG) {
+    const uint64_t R16 = (uint64_t)d.nblk * (Lb / 16);
+    const uint64_t r0 = R16 * gi / gn * 16, r1 = R16 * (gi + 1) / gn * 16;
+    if (r0 >= r1) return;
+    for (int v = 0; v < p.V; ++v)
+      for (uint64_t f = r0 / Lb; f * Lb < r1; ++f) {
+        const uint64_t a = r0 > f * Lb ? r0 - f * Lb : 0;
+        const uint64_t e = r1 - f * Lb < Lb ? r1 - f * Lb : Lb;
+        fn((uint64_t)v * d.nblk + f, a, e);
+      }
+    return;
+  }
+  const uint64_t tot16 = unit_items(p, d, mode) * (Lb / 16);
+  const uint64_t u0 = tot16 * gi / gn * 16, u1 = tot16 * (gi + 1) / gn * 16;
+  for (uint64_t it = u0 / Lb; it * Lb < u1; ++it) {
+    const uint64_t a = u0 > it * Lb ? u0 - it * Lb : 0;
+    const uint64_t e = u1 - it * Lb < Lb ? u1 - it * Lb : Lb;
+    fn(it, a, e);
+  }
+}
+
+__device__ __forceinline__ bool unit_has_work(const KParams& p, const OpDesc& d, int mode, int gi, int gn) {
+  const uint64_t Lb16 = p.slice_elems * p.elem_size / 16;
+  if (mode == U_RING_RS || mode == U_RING_AG) {
+    const uint64_t R16 = (uint64_t)d.nblk * Lb16;
+    return R16 * (gi + 1) / gn > R16 * gi / gn;
+  }
+  const uint64_t tot16 = unit_items(p, d, mode) * Lb16;
+  return tot16 * (gi + 1) / gn > tot16 * gi / gn;
+}
+
+// sources of a unit's item, in summation order
+__device__ __forceinline__ int unit_nsrc(const KParams& p, const OpDesc& d, int mode) {
+  return mode == U_DIRECT_RS ? p.size[d.dim] : mode == U_RING_RS ? 2 : 1;
+}
+__device__ __forceinline__ int unit_src_rank(const KParams& p, const OpDesc& d, int mode, const Item& m, int j) {
+  const int k = d.dim;
+  switch (mode) {
+    case U_DIRECT_RS: return m.g0 + j * (int)p.stride[k];
+    case U_DIRECT_AG: return m.g0 + m.j * (int)p.stride[k];
+    case U_RING_RS: return j == 0 ? ring_peer(p, m.q, k, -1) : m.q;  // left partial + own value
+    default: return ring_peer(p, m.q, k, -1);
+  }
+}
+
+// Address of dim-k member j's copy of the current piece (LDG path).
+struct PeerSrc {
+  const KParams* p;
+  int q0, step;
+  uint64_t off;
+  __device__ __forceinline__ const uint4* operator()(int j) const {
+    return reinterpret_cast<const uint4*>(data_of(*p, q0 + j * step) + off);
+  }
+};
+
+// ------------------------------------------------------- path 1: LDG / STG
+// Direct algorithm only: every thread issues NSRC*UNROLL 16-byte L1-bypassing
+// loads before adding.  (Ring dims need the TMA engine.)
+template <class Tag>
+__device__ void run_op_ldg(const KParams& p, const OpDesc& d, int gi, int gn) {
+  const int k = d.dim, pk = p.size[k];
+  const int mode = unit_mode(d);
+  const uint64_t Lv = p.slice_elems * p.elem_size / 16;
+  for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+    const Item m = decode_item(p, d, mode, 0, it);
+    uint4* dst = reinterpret_cast<uint4*>(data_of(p, m.q) + m.off);
+    const PeerSrc src{&p, m.g0, (int)p.stride[k], m.off};
+    (void)Lv;
+    if (mode == U_DIRECT_AG) {
+      dev::copy_range<8>(dst, src(m.j), a / 16, e / 16);
+      return;
+    }
+    switch (pk) {
+      case 2: dev::reduce_range<Tag, 2, 4>(dst, src, a / 16, e / 16); break;
+      case 3: dev::reduce_range<Tag, 3, 4>(dst, src, a / 16, e / 16); break;
+      case 4: dev::reduce_range<Tag, 4, 2>(dst, src, a / 16, e / 16); break;
+      case 8: dev::reduce_range<Tag, 8, 1>(dst, src, a / 16, e / 16); break;
+      default: dev::reduce_range_generic<Tag>(dst, src, pk, a / 16, e / 16); break;
+    }
+  });
+}
+
+// ------------------------------------------------------- path 2: TMA bulk
+// Warp-specialised CTA: warp 0 = producer (one lane streams each tile's
+// sources into a kStages-deep shared-memory ring with cp.async.bulk, local HBM
+// or a peer's HBM over NVLink), warps 1..8 = consumers (sum in order / pass
+// through, 16-byte STG), warp 9 = completion (counts and publishes).
+constexpr int kStages = 6;
+constexpr int kStageBytes = 32 * 1024;
+constexpr int kConsumerWarps = 8;
+constexpr int kOpRing = 16;  // units the consumers may run ahead of the completion warp
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * (kStages + kOpRing) * 8;
+static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + completion warp");
+
+__device__ __forceinline__ uint32_t unit_tile(int nsrc) { return ((uint32_t)kStageBytes / nsrc) & ~15u; }
+
+// Producer (one lane): stream this CTA's tiles of one unit into the ring.
+__device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
+                                             char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
+                                             uint64_t t_op, double& sent) {
+  const int nsrc = unit_nsrc(p, d, mode);
+  const uint32_t tile = unit_tile(nsrc);
+  const float pace = p.pace_ns_per_byte[d.dim];
+  const int remote = mode == U_DIRECT_RS ? p.size[d.dim] - 1 : 1;  // peer sources per tile
+  dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
+  for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+    const Item m = decode_item(p, d, mode, step, it);
+    const char* src[THEMIS_MAX_DIMS > 8 ? THEMIS_MAX_DIMS : 8];
+    const int ns = nsrc <= 8 ? nsrc : 8;
+    for (int j = 0; j < ns; ++j) src[j] = data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off;
+    for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
+      const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
+      if (pace > 0.f) {  // absolute due times from the group's op origin
+        const uint64_t due = t_op + (uint64_t)(sent * pace);
+        while (dev::globaltimer() < due) {
+        }
+        sent += (double)bytes * remote;
+      }
+      const int s = ctr % p.stages;
+      dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+      dev::mbar_expect_tx(&full[s], bytes * nsrc);
+      char* dst = smem + s * kStageBytes;
+      for (int j = 0; j < nsrc; ++j) {
+        const char* sj = j < 8 ? src[j] : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off;
+        dev::bulk_g2s(dst + j * tile, sj + pos, bytes, &full[s]);
+      }
+    }
+  });
+}
+
+// Consumers: returns false if the kernel is aborting (watchdog).
+template <class Tag>
+__device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
+                                             const char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+  const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
+  constexpr int kCons = 32 * kConsumerWarps;
+  const int nsrc = unit_nsrc(p, d, mode);
+  const uint32_t tile = unit_tile(nsrc), tile16 = tile / 16;
+  const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
+  bool ok = true;
+  for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+    if (!ok) return;
+    const Item m = decode_item(p, d, mode, step, it);
+    char* base = data_of(p, m.q) + m.off;
+    for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
+      const uint32_t n16 = (uint32_t)((e - pos < tile ? e - pos : tile) / 16);
+      const int s = ctr % p.stages;
+      if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) {
+        ok = false;
+        return;
+      }
+      const uint4* sm = reinterpret_cast<const uint4*>(smem + s * kStageBytes);
+      uint4* dst = reinterpret_cast<uint4*>(base + pos);
+      if (reduce) {
+        for (uint32_t w = ct; w < n16; w += kCons) {
+          float acc[Tag::kAcc];
+          Tag::load(acc, sm[w]);
+          for (int j = 1; j < nsrc; ++j) Tag::add(acc, sm[j * tile16 + w]);
+          dev::st_v4(dst + w, Tag::store(acc));
+        }
+      } else {
+        for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
+    }
+  });
+  return ok;
+}
+
+// One warp: wait until the local ranks and their dim-k peers completed (c, s-1).
+__device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d, int opi) {
+  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
+  bool ok = true;
+  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
+    const int q = q0 + t / pk;
+    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+  }
+  return __all_sync(0xFFFFFFFFu, ok);
+}
+
+__device__ __forceinline__ unsigned long long ring_flag_value(uint32_t epoch, int seq, int steps_done) {
+  return ((unsigned long long)epoch << 32) | ((unsigned long long)seq << 8) | (unsigned long long)steps_done;
+}
+
+// One warp: ring step `step` (>= 1) of CTA gi needs the left neighbours' CTA gi
+// to have finished step - 1 of the same op.
+__device__ __forceinline__ bool wait_ring_warp(const KParams& p, const OpDesc& d, int step, int gi) {
+  const int V = p.V, q0 = p.my_gpu * V, k = d.dim;
+  bool ok = true;
+  for (int v = threadIdx.x & 31; v < V; v += 32) {
+    const int q = q0 + v;
+    ok &= wait_geq64(p, ring_slot(p, q, ring_peer(p, q, k, -1), k, gi), ring_flag_value(p.epoch, d.seq, step),
+                     0xFFFFFCu);
+  }
+  return __all_sync(0xFFFFFFFFu, ok);
+}
+
+// One warp: this CTA finished ring step `step` -> tell the right neighbours.
+__device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc& d, int step, int gi) {
+  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, lane = threadIdx.x & 31;
+  if (lane == 0) dev::fence_acq_rel_sys();
+  __syncwarp();
+  for (int v = lane; v < V; v += 32) {
+    const int q = q0 + v;
+    dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(p.epoch, d.seq, step + 1));
+  }
+  __syncwarp();
+}
+
+// One warp: count this CTA's completion of op opi; the group's last CTA
+// publishes the epoch to the consumers of (c, s): self and the next stage's
+// dim peers.  Release chain: consumers' stores -> mbarrier arrive (release.cta)
+// / bar.sync -> atom.acq_rel.gpu (all CTAs) -> fence.acq_rel.sys -> relaxed
+// sys stores.
+__device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc& d, int opi, int gn) {
+  const int lane = threadIdx.x & 31;
+  uint32_t last = 0;
+  if (lane == 0) {
+    last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
+    if (last) {
+      p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
+      p.op_t0[opi] = 0;
+      dev::fence_acq_rel_sys();
+    }
+  }
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  if (d.next_dim >= 0) {
+    const int V = p.V, q0 = p.my_gpu * V, kn = d.next_dim, pn = p.size[kn];
+    for (int t = lane; t < V * pn; t += 32) {
+      const int q = q0 + t / pn;
+      const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
+      dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
+    }
+  }
+  if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
+  __syncwarp();
+}
+
+template <class Tag, bool kTma>
+__global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(128) char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* op_done = empty + kStages;
+  uint64_t* op_free = op_done + kOpRing;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int g = 0;
+  while (g + 1 < p.D && (int)blockIdx.x >= p.grp_start[g + 1]) ++g;
+  const int gi = blockIdx.x - p.grp_start[g];
+  const int gn = p.grp_start[g + 1] - p.grp_start[g];
+  const int V = p.V, P = p.P;
+  const int q0 = p.my_gpu * V;
+  bool ok = true;
+  if (kTma && tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < kOpRing; ++s) {
+      dev::mbar_init(&op_done[s], kConsumerWarps);
+      dev::mbar_init(&op_free[s], 1);
+    }
+    dev::fence_mbar_init();
+  }
+
+  // a6: entry barrier — every local rank announces the epoch to every rank.
+  if (blockIdx.x == 0)
+    for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), p.epoch);
+  for (int i = tid; i < V * P; i += blockDim.x)
+    ok &= wait_geq(p, entry_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFFu);
+  ok = __syncthreads_and(ok);
+
+  // a9: walk this dimension's ops in the enforced order.
+  const int* list = p.dim_ops + (uint64_t)g * p.C * p.NS;
+  const int nops = ok ? p.dim_ops_n[g] : 0;
+  if constexpr (kTma) {
+    // Decoupled: the producer waits for a unit's dependencies and streams its
+    // tiles, then moves on while the consumers finish; the completion warp
+    // counts and publishes, so no sys fence ever stalls the tile stream.
+    uint32_t ctr = 0;  // ring position (identical sequence in producer and consumers)
+    if (warp == 0) {
+      for (int i = 0; i < nops; ++i) {
+        const int opi = list[i];
+        const OpDesc& d = p.ops[opi];
+        const int mode = unit_mode(d);
+        const int nu = d.ring ? p.size[d.dim] - 1 : 1;
+        if (!unit_has_work(p, d, mode, gi, gn)) continue;  // nothing to wait for or move
+        uint64_t t_op = 0;
+        double sent = 0.0;
+        bool stop = false;
+        for (int u = 0; u < nu && !stop; ++u) {
+          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
+            stop = true;
+            break;
+          }
+          if (lane == 0) {
+            if (u == 0) {
+              if (p.trace && gi == 0) p.trace[2 * opi] = dev::globaltimer();
+              if (p.pace_ns_per_byte[d.dim] > 0.f) {  // group-shared pacing origin (first starter wins)
+                const unsigned long long now = dev::globaltimer();
+                const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
+                t_op = prev ? prev : now;
+              }
+            }
+            produce_unit(p, d, mode, u, gi, gn, smem, full, empty, ctr, t_op, sent);
+          }
+          __syncwarp();
+        }
+        if (stop) break;
+      }
+    } else if (warp <= kConsumerWarps) {
+      // consumers: per unit, every consumer warp arrives on op_done[slot]
+      // (mbarrier arrive = release.cta of its stores) after the completion
+      // warp has freed that slot (ring of kOpRing units).
+      int n = 0;
+      bool run = true;
+      for (int i = 0; i < nops && run; ++i) {
+        const int opi = list[i];
+        const OpDesc& d = p.ops[opi];
+        const int mode = unit_mode(d);
+        const int nu = d.ring ? p.size[d.dim] - 1 : 1;
+        for (int u = 0; u < nu; ++u, ++n) {
+          if (!consume_unit<Tag>(p, d, mode, u, gi, gn, smem, full, empty, ctr)) {
+            run = false;
+            break;
+          }
+          __syncwarp();
+          bool w = true;
+          if (lane == 0) {
+            const int slot = n % kOpRing;
+            w = dev::mbar_wait_or(&op_free[slot], ((n / kOpRing) & 1) ^ 1, p.abort_flag);
+            if (w) dev::mbar_arrive(&op_done[slot]);
+          }
+          if (!__shfl_sync(0xFFFFFFFFu, w, 0)) {
+            run = false;
+            break;
+          }
+        }
+      }
+    } else {
+      // completion warp: ring steps publish per-CTA step flags; the last unit
+      // of an op counts group-wide and publishes the op's ready flags.
+      int n = 0;
+      bool run = true;
+      for (int i = 0; i < nops && run; ++i) {
+        const int opi = list[i];
+        const OpDesc& d = p.ops[opi];
+        const int mode = unit_mode(d);
+        const int nu = d.ring ? p.size[d.dim] - 1 : 1;
+        const bool work = unit_has_work(p, d, mode, gi, gn);
+        for (int u = 0; u < nu; ++u, ++n) {
+          const int slot = n % kOpRing;
+          bool w = true;
+          if (lane == 0) w = dev::mbar_wait_or(&op_done[slot], (n / kOpRing) & 1, p.abort_flag);
+          if (!__shfl_sync(0xFFFFFFFFu, w, 0)) {
+            run = false;
+            break;
+          }
+          if (u + 1 < nu) {
+            if (work) publish_ring_warp(p, d, u, gi);
+          } else {
+            complete_op_warp(p, d, opi, gn);
+          }
+          if (lane == 0) dev::mbar_arrive(&op_free[slot]);
+        }
+      }
+    }
+  } else {
+    for (int i = 0; ok && i < nops; ++i) {
+      const int opi = list[i];
+      const OpDesc& d = p.ops[opi];
+      const int k = d.dim;
+      if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
+        const int pk = p.size[k];
+        for (int t = tid; t < V * pk; t += blockDim.x) {
+          const int q = q0 + t / pk;
+          const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+        }
+        ok = __syncthreads_and(ok);
+        if (!ok) break;
+      }
+      if (p.trace && gi == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
+      run_op_ldg<Tag>(p, d, gi, gn);
+      __syncthreads();
+      if (warp == 0) complete_op_warp(p, d, opi, gn);
+      __syncthreads();
+    }
+  }
+
+  // exit: all CTAs done -> exit barrier so no peer still reads our buffers.
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    atomicAdd(p.done_cnt, 1u);
+  }
+  if (blockIdx.x != 0) return;
+  if (tid == 0) {
+    ok &= wait_geq(p, p.done_cnt, gridDim.x, 0xFFFFFEu);
+    *p.done_cnt = 0;
+    __threadfence_system();
+  }
+  __syncthreads();
+  for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(exit_slot(p, i % P, q0 + i / P), p.epoch);
+  for (int i = tid; i < V * P; i += blockDim.x) wait_geq(p, exit_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFDu);
+}

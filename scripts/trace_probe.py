@@ -58,5 +58,24 @@ for k, ops in enumerate(plan.dim_ops()):
           f"first start {starts[0]/1e3:.1f} last end {ends[-1]/1e3:.1f}; gap mean {gaps.mean()/1e3:.2f} "
           f"max {gaps.max()/1e3:.2f} us; op dur/model mean {np.mean(dur/mdur):.3f} min {np.min(dur/mdur):.3f}")
     print("   first ops (dur us, model us):", [(round(d / 1e3, 1), round(m / 1e3, 1)) for d, m in zip(dur[:6], mdur[:6])])
+lat = []
+for c in range(plan.info["n_chunks"]):
+    for s in range(1, NS):
+        lat.append(tr[c, s, 0] - tr[c, s - 1, 1])
+lat = np.array(lat)
+print(f"stage transition (start(c,s) - end(c,s-1)) us: p10 {np.percentile(lat,10)/1e3:.2f} median "
+      f"{np.median(lat)/1e3:.2f} p90 {np.percentile(lat,90)/1e3:.2f} min {lat.min()/1e3:.2f}")
+# per-dim idle while the dim still has pending ops (model idle_K analogue)
+for k, ops in enumerate(plan.dim_ops()):
+    iv = sorted((tr[c, s, 0], tr[c, s, 1]) for c, s in ops)
+    busy, cur_s, cur_e = 0, iv[0][0], iv[0][1]
+    for a_, b_ in iv[1:]:
+        if a_ > cur_e:
+            busy += cur_e - cur_s
+            cur_s, cur_e = a_, b_
+        else:
+            cur_e = max(cur_e, b_)
+    busy += cur_e - cur_s
+    print(f"dim{k+1}: union-busy {busy/1e3:.1f} us of span {(iv[-1][1]-iv[0][0])/1e3:.1f} us")
 plan.close()
 comm.close()

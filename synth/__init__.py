@@ -21,16 +21,26 @@ DTYPES = ("f32", "bf16", "f16", "i32")
 ELEM_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4}
 
 
-def host_inputs(P: int, count: int, dtype: str, seed: int = SEED_BASE) -> list:
-    """Per-rank numpy inputs.  bf16 is returned as uint16 bit patterns."""
+def host_inputs(P: int, count: int, dtype: str, seed: int = SEED_BASE, dist: str = "recipe") -> list:
+    """Per-rank numpy inputs.  bf16 is returned as uint16 bit patterns.
+    dist="wide": N(0,1) * 2^U{-8..8} for floats — magnitudes spread over 16
+    binades so that sums are inexact and the summation order shows in the
+    bits (U[-1,1) fp32 values are multiples of 2^-23: 2-3 term sums are exact)."""
     import torch
     out = []
     for r in range(P):
         g = torch.Generator(device="cpu")
         g.manual_seed(seed + r)
-        out.append(_draw(count, dtype, g, "cpu").numpy().copy() if dtype != "bf16"
-                   else _draw(count, dtype, g, "cpu").view(torch.int16).numpy().view(np.uint16).copy())
+        x = _draw_wide(count, dtype, g) if (dist == "wide" and dtype != "i32") else _draw(count, dtype, g, "cpu")
+        out.append(x.numpy().copy() if dtype != "bf16" else x.view(torch.int16).numpy().view(np.uint16).copy())
     return out
+
+
+def _draw_wide(count, dtype, g):
+    import torch
+    x = torch.randn(count, generator=g, dtype=torch.float32)
+    e = torch.randint(-8, 9, (count,), generator=g).to(torch.float32)
+    return (x * torch.exp2(e)).to(torch_dtype(dtype))
 
 
 def device_input(rank: int, count: int, dtype: str, device, seed: int = SEED_BASE):

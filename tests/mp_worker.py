@@ -18,8 +18,11 @@ from synth import ELEM_SIZE, host_inputs  # noqa: E402
 COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
 
 
-def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine):
-    topo = th.Topology(sizes, bw)
+KIND_O = {th.RING: T.RING, th.DIRECT: T.DIRECT, th.SWITCH: T.SWITCH}
+
+
+def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None):
+    topo = th.Topology(sizes, bw, kinds)
     P = topo.P
     V = P // W
     N = P * C * slice_elems
@@ -28,7 +31,7 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine):
     comm.set_engine(engine)
     comm.set_timeout(20.0)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy).bind(comm)
-    xs = host_inputs(P, N, dtype)
+    xs = host_inputs(P, N, dtype, dist="wide")
     for v in range(V):
         r = g * V + v
         src = torch.from_numpy(xs[r].view(np.int16) if dtype == "bf16" else xs[r])
@@ -38,7 +41,7 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine):
     th.run(COLL[coll], comm, plan, N, dtype)
     torch.cuda.synchronize()
     comm.status()
-    o = T.Topology.make(sizes, bw)
+    o = T.Topology.make(sizes, bw, [KIND_O[k] for k in kinds] if kinds else None)
     sched = S.schedule_collective(o, coll, N * esz, C, S.THEMIS if policy == th.THEMIS else S.BASELINE)
     want = O.run_schedule(xs, sched, dtype)
     bad = []
@@ -70,7 +73,11 @@ def main():
               ((2, 2, 2), (1, 1, 1), "i32", 4, 2048, "AG", th.THEMIS, "tma"),
               ((W,), (1,), "f32", 4, 8196, S.AR, th.THEMIS, "tma"),
               ((2, 4), (1, 1), "f32", 16, 1028, S.AR, th.THEMIS, "tma"),
-              ((4, 2), (1, 1), "i32", 16, 1028, S.AR, th.THEMIS, "tma")]
+              ((4, 2), (1, 1), "i32", 16, 1028, S.AR, th.THEMIS, "tma"),
+              ((W,), (1,), "f32", 4, 8196, S.AR, th.THEMIS, "tma", (th.RING,)),
+              ((2, 2, 2), (1, 1, 1), "f32", 4, 4100, S.AR, th.THEMIS, "tma", (th.RING,) * 3),
+              ((2, 4), (1, 1), "f32", 8, 2052, S.AR, th.THEMIS, "tma", (th.DIRECT, th.RING)),
+              ((4, 2), (1, 1), "f32", 8, 2052, "RS", th.THEMIS, "tma", (th.RING, th.DIRECT))]
     fails = []
     for c in cases:
         if int(np.prod(c[0])) % W:

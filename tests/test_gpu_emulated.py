@@ -31,14 +31,18 @@ def _gpu():
     torch.cuda.set_device(0)
 
 
-def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF):
-    o = T.Topology.make(sizes, [b for b in bw])
+KIND_O = {th.RING: T.RING, th.DIRECT: T.DIRECT, th.SWITCH: T.SWITCH}
+
+
+def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
+    ok = [KIND_O[k] for k in kinds] if kinds else None
+    o = T.Topology.make(sizes, [b for b in bw], ok)
     return S.schedule_collective(o, coll, nbytes, C, S.THEMIS if policy == th.THEMIS else S.BASELINE)
 
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
-             intra=th.SCF, repeat=1):
-    topo = th.Topology(tuple(sizes), tuple(bw))
+             intra=th.SCF, repeat=1, kinds=None, dist="recipe"):
+    topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
     esz = ELEM_SIZE[dtype]
@@ -47,7 +51,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_timeout(10.0)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra).bind(comm, ctas)
     try:
-        xs = host_inputs(P, N, dtype)
+        xs = host_inputs(P, N, dtype, dist=dist)
         for it in range(repeat):
             for r in range(P):
                 v = comm.rank_view(r, N, dtype)
@@ -77,7 +81,7 @@ def check_ar(sizes, bw, dtype, C, slice_elems, policy=th.THEMIS, **kw):
         for r in range(P):
             assert np.array_equal(outs[r], want), f"rank {r}"
         return
-    sched = oracle_sched(sizes, bw, S.AR, N * ELEM_SIZE[dtype], C, policy)
+    sched = oracle_sched(sizes, bw, S.AR, N * ELEM_SIZE[dtype], C, policy, kinds=kw.get("kinds"))
     tree = O.run_schedule(xs, sched, dtype)
     ref = O.allreduce_definition(xs, dtype)
     scale = O.abs_sum(xs, dtype)
@@ -103,6 +107,50 @@ def test_allreduce_int32_exact(sizes, bw):
 @pytest.mark.parametrize("policy", [th.THEMIS, th.BASELINE])
 def test_allreduce_float_bitexact_vs_oracle(dtype, policy):
     check_ar((2, 2, 2), (1, 1, 1), dtype, 8, RAGGED[dtype], policy)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_allreduce_wide_values_order_sensitive(dtype):
+    """Magnitudes over 16 binades make every float sum inexact, so bit-exactness
+    against the oracle checks the summation order (R18) itself."""
+    check_ar((2, 2, 2), (1, 1, 1), dtype, 8, RAGGED[dtype], dist="wide")
+    check_ar((4, 2), (1, 1), dtype, 4, RAGGED[dtype], dist="wide")
+
+
+R, Dk = th.RING, th.DIRECT
+
+
+@pytest.mark.parametrize("sizes,kinds", [((3,), (R,)), ((4,), (R,)), ((8,), (R,)), ((4, 2), (R, Dk)),
+                                         ((2, 4), (Dk, R)), ((3, 2, 2), (R, Dk, R)), ((2, 3, 2), (Dk, R, Dk))])
+def test_ring_dimensions(sizes, kinds):
+    """Table 1 Ring dims run the ring algorithm (P_k - 1 neighbour steps,
+    PAPER.md:214/:234/:477): int32 exact and f32 bit-exact against the oracle's
+    ring summation order."""
+    bw = (1,) * len(sizes)
+    check_ar(sizes, bw, "i32", 4, 2052, kinds=kinds)
+    check_ar(sizes, bw, "f32", 4, RAGGED["f32"], kinds=kinds, dist="wide")
+    check_ar(sizes, bw, "f32", 2, 4100, kinds=kinds, dist="wide", ctas=[3] * len(sizes))
+
+
+def test_ring_reduce_scatter_all_gather():
+    sizes, kinds, C = (4, 2), (R, Dk), 4
+    xs, outs = run_case(sizes, (1, 1), "f32", C, 4096, "RS", kinds=kinds, dist="wide")
+    N, P = xs[0].shape[0], 8
+    sched = oracle_sched(sizes, (1, 1), "RS", N * 4, C, th.THEMIS, kinds=kinds)
+    tree = O.run_schedule(xs, sched, "f32")
+    blk = N // P
+    for r in range(P):
+        assert np.array_equal(outs[r][r * blk:(r + 1) * blk], tree[r][r * blk:(r + 1) * blk])
+    xs, outs = run_case(sizes, (1, 1), "i32", C, 4096, "AG", kinds=kinds)
+    cat = O.all_gather_definition(xs, P)
+    for r in range(P):
+        assert np.array_equal(outs[r], cat)
+
+
+def test_ring_needs_tma_engine():
+    with pytest.raises(th.ThemisError) as e:
+        run_case((3,), (1,), "i32", 2, 1024, kinds=(R,), engine="ldg")
+    assert e.value.status == 1
 
 
 def test_allreduce_ldg_engine():

@@ -169,3 +169,41 @@ def test_rejects_bad_sizes():
     x = [np.zeros(6, np.int32)] * 4
     with pytest.raises(ValueError):
         O.run_schedule(x, _sched(t, S.AR, 6, 4, 1, [(0, 1)]), "i32")
+
+
+def _ring_rs_message_passing(parts, dtype_add):
+    """Step-by-step ring Reduce-Scatter as in the paper's RingAllReduce figure
+    (PAPER.md:214): P-1 steps; in each step every NPU sends one partial to its
+    right neighbour, which adds its own copy.  parts[m][t] = member m's part t.
+    Returns owner t's final part t (the chain ends at the owner)."""
+    P = len(parts)
+    partial = {}
+    # step 0: member m sends its own part (m - 1) mod P to m + 1
+    for m in range(P):
+        t = (m - 1) % P
+        partial[((m + 1) % P, t)] = parts[m][t]
+    for _ in range(1, P - 1):
+        nxt = {}
+        for (m, t), v in partial.items():
+            nxt[((m + 1) % P, t)] = dtype_add(v, parts[m][t])
+        partial = nxt
+    return [dtype_add(partial[(t, t)], parts[t][t]) for t in range(P)]
+
+
+def test_ring_summation_order_matches_message_passing():
+    """The oracle's ring RS (closed-form member order) equals an explicit
+    message-passing ring on floats, bit for bit (order matters for floats)."""
+    for P in (3, 4, 5):
+        t = T.Topology.make((P,), (1,), (T.RING,))
+        N = P * 16
+        x = host_inputs(P, N, "f32", seed=77 + P, dist="wide")
+        out = O.run_schedule(x, _sched(t, "RS", N, 4, 1, [(0,)]), "f32")
+        blk = N // P
+        parts = [[x[m][q * blk:(q + 1) * blk] for q in range(P)] for m in range(P)]
+        want = _ring_rs_message_passing(parts, lambda a, b: (a + b).astype(np.float32))
+        for r in range(P):
+            assert np.array_equal(out[r][r * blk:(r + 1) * blk], want[r])
+        # direct order differs for P >= 3 in general (coordinate order)
+        td = T.Topology.make((P,), (1,), (T.DIRECT,))
+        outd = O.run_schedule(x, _sched(td, "RS", N, 4, 1, [(0,)]), "f32")
+        assert any(not np.array_equal(outd[r][r * blk:(r + 1) * blk], want[r]) for r in range(P))
