@@ -85,10 +85,14 @@ def check_ar(sizes, bw, dtype, C, slice_elems, policy=th.THEMIS, **kw):
     tree = O.run_schedule(xs, sched, dtype)
     ref = O.allreduce_definition(xs, dtype)
     scale = O.abs_sum(xs, dtype)
+    # north_star tolerance on the recipe inputs; on the adversarial "wide"
+    # inputs the F10 worst-case bound (one RNE per RS stage: D * 2^-8 for bf16)
+    tol = TOL[dtype] if kw.get("dist", "recipe") == "recipe" else max(TOL[dtype], len(sizes) * 2.0 ** -8 if
+                                                                      dtype == "bf16" else TOL[dtype])
     for r in range(P):
         assert np.array_equal(outs[r].view(np.uint8), tree[r].view(np.uint8)), f"rank {r} not bit-exact"
         err = np.abs(O.to_f64(outs[r], dtype) - ref)
-        assert np.all(err <= TOL[dtype] * scale)
+        assert np.all(err <= tol * scale)
 
 
 # slice_elems chosen so one slice spans several 32 KiB TMA tiles plus a ragged
