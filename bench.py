@@ -314,11 +314,14 @@ def run_themis(a):
                 "algorithmic_bytes_per_launch": nvl_bytes,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"}
     roof["kernel"] = "themis_exec_kernel<F32Tag,true> (TMA engine)"
-    if os.environ.get("THEMIS_TRAFFIC_JSON"):
-        try:
-            roof["traffic"] = json.load(open(os.environ["THEMIS_TRAFFIC_JSON"])).get(str(world))
-        except Exception:
-            pass
+    try:   # ncu-measured DRAM bytes per launch for this exact config (profiles/ncu_traffic.json)
+        key = f"n{world}_{'x'.join(map(str, SIZES))}_{a.mib}MiB_c{a.chunks}_{a.ratio}"
+        ent = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(key)
+        if ent and roof["bound"] == "hbm":
+            roof["traffic"] = ent["traffic"]
+            roof["traffic_source"] = ent["source"]
+    except Exception:
+        pass
 
     cpu = None
     if world == 1 and not a.no_cpu:
