@@ -121,6 +121,16 @@ typedef struct themis_comm themis_comm_t;
  * (themis_plan_free). */
 themis_status_t themis_plan(const themis_topology_t* topo /*[host]*/, const themis_plan_req_t* req /*[host]*/,
                             themis_plan_t** out /*[out]*/);
+/* themis_plan_custom: a plan whose per-chunk dim orders are given by the
+ * caller instead of Algorithm 1 — any RS order x any AG order per chunk
+ * (Observations 1-2; e.g. a brute-force optimum, or a
+ * projection of a larger topology's schedule).  rs_order / ag_order: [host]
+ * C*D 0-based dims, row-major (rs_order may be NULL for AG, ag_order NULL
+ * for RS).  The intra-dimension order is pre-simulated as in themis_plan;
+ * req->policy is ignored.  Errors: INVALID_ARG (not a permutation, missing
+ * order), OVERFLOW. */
+themis_status_t themis_plan_custom(const themis_topology_t* topo /*[host]*/, const themis_plan_req_t* req /*[host]*/,
+                                   const uint8_t* rs_order, const uint8_t* ag_order, themis_plan_t** out /*[out]*/);
 themis_status_t themis_plan_info(const themis_plan_t* plan, themis_plan_info_t* info /*[host, out]*/);
 /* Per-chunk dim orders, 0-based dims, row-major [C][D]; ag_order for AR is
  * reverse(rs_order) (Algorithm 1 line 8).  RS plans leave ag_order rows 0xFF,

@@ -51,6 +51,7 @@ _P = C.c_void_p
 _ST = C.c_int
 SIGNATURES = {
     "themis_plan": (_ST, [C.POINTER(Topology_t), C.POINTER(PlanReq_t), C.POINTER(_P)]),
+    "themis_plan_custom": (_ST, [C.POINTER(Topology_t), C.POINTER(PlanReq_t), _P, _P, C.POINTER(_P)]),
     "themis_plan_info": (_ST, [_P, C.POINTER(PlanInfo_t)]),
     "themis_plan_orders": (_ST, [_P, _P, _P]),
     "themis_plan_dim_ops": (_ST, [_P, _P, _P]),

@@ -195,6 +195,44 @@ struct Planner {
     pl.load.assign(L, L + D);
   }
 
+  // Caller-given per-chunk orders (any of the D! x D! per chunk):
+  // the tracker is only walked (reported as final_load); n_greedy counts the
+  // chunks whose order differs from the baseline.
+  void custom_orders(const uint8_t* rs_in, const uint8_t* ag_in) {
+    const int coll = pl.req.coll;
+    u128 L[THEMIS_MAX_DIMS];
+    for (int k = 0; k < D; ++k)
+      L[k] = coll == THEMIS_ALLREDUCE ? A_rs[k] + A_ag[k] : coll == THEMIS_REDUCE_SCATTER ? A_rs[k] : A_ag[k];
+    const u128 chunk = chunk_scaled();
+    pl.rs.assign((size_t)C * D, 0xFF);
+    pl.ag.assign((size_t)C * D, 0xFF);
+    pl.n_greedy = 0;
+    for (int c = 0; c < C; ++c) {
+      u128 inc[THEMIS_MAX_DIMS] = {0};
+      uint8_t* rs = &pl.rs[(size_t)c * D];
+      uint8_t* ag = &pl.ag[(size_t)c * D];
+      bool differs = false;
+      u128 b = coll == THEMIS_ALL_GATHER ? chunk / P : chunk;
+      if (coll != THEMIS_ALL_GATHER) {
+        for (int k = 0; k < D; ++k) {
+          rs[k] = rs_in[(size_t)c * D + k];
+          differs |= rs[k] != k;
+        }
+        walk(0, rs, b, inc, &b);
+      }
+      if (coll != THEMIS_REDUCE_SCATTER) {
+        for (int k = 0; k < D; ++k) {
+          ag[k] = ag_in[(size_t)c * D + k];
+          differs |= ag[k] != D - 1 - k;
+        }
+        walk(1, ag, b, inc, nullptr);
+      }
+      pl.n_greedy += differs;
+      for (int k = 0; k < D; ++k) L[k] += inc[k];
+    }
+    pl.load.assign(L, L + D);
+  }
+
   void build_ops() {
     const int coll = pl.req.coll;
     pl.NS = coll == THEMIS_ALLREDUCE ? 2 * D : D;
@@ -324,12 +362,27 @@ bool fits64(u128 v) { return v <= (u128)UINT64_MAX; }
 
 using namespace themis;
 
-extern "C" themis_status_t themis_plan(const themis_topology_t* topo, const themis_plan_req_t* req,
-                                       themis_plan_t** out) {
+static themis_status_t build_plan(const themis_topology_t* topo, const themis_plan_req_t* req, const uint8_t* rs,
+                                  const uint8_t* ag, bool custom, themis_plan_t** out) {
   if (!out) return fail(THEMIS_ERR_INVALID_ARG, "out is null");
   *out = nullptr;
   themis_status_t st = validate(topo, req);
   if (st != THEMIS_OK) return st;
+  if (custom) {  // every given order must be a permutation of the dims
+    const int D = topo->ndims, C = req->n_chunks;
+    const bool need_rs = req->coll != THEMIS_ALL_GATHER, need_ag = req->coll != THEMIS_REDUCE_SCATTER;
+    if ((need_rs && !rs) || (need_ag && !ag)) return fail(THEMIS_ERR_INVALID_ARG, "missing rs_order / ag_order");
+    for (int c = 0; c < C; ++c)
+      for (const uint8_t* o : {need_rs ? rs : nullptr, need_ag ? ag : nullptr}) {
+        if (!o) continue;
+        uint32_t seen = 0;
+        for (int k = 0; k < D; ++k) {
+          const uint8_t d = o[(size_t)c * D + k];
+          if (d >= D || (seen >> d & 1u)) return fail(THEMIS_ERR_INVALID_ARG, "order is not a permutation of the dims");
+          seen |= 1u << d;
+        }
+      }
+  }
   try {
     auto* pl = new themis_plan_t();
     std::memset(&pl->topo, 0, sizeof(pl->topo));
@@ -350,7 +403,10 @@ extern "C" themis_status_t themis_plan(const themis_topology_t* topo, const them
       delete pl;
       return st;
     }
-    p.algorithm1();
+    if (custom)
+      p.custom_orders(rs, ag);
+    else
+      p.algorithm1();
     p.build_ops();
     p.simulate();
     p.hash();
@@ -365,6 +421,16 @@ extern "C" themis_status_t themis_plan(const themis_topology_t* topo, const them
   } catch (const std::exception& e) {
     return fail(THEMIS_ERR_INVALID_ARG, std::string("planner: ") + e.what());
   }
+}
+
+extern "C" themis_status_t themis_plan(const themis_topology_t* topo, const themis_plan_req_t* req,
+                                       themis_plan_t** out) {
+  return build_plan(topo, req, nullptr, nullptr, false, out);
+}
+
+extern "C" themis_status_t themis_plan_custom(const themis_topology_t* topo, const themis_plan_req_t* req,
+                                              const uint8_t* rs_order, const uint8_t* ag_order, themis_plan_t** out) {
+  return build_plan(topo, req, rs_order, ag_order, true, out);
 }
 
 extern "C" themis_status_t themis_plan_info(const themis_plan_t* pl, themis_plan_info_t* info) {

@@ -70,14 +70,27 @@ class Plan:
     """A Themis (or baseline) plan: per-chunk dim orders + per-dim op order."""
 
     def __init__(self, topo: Topology, coll: int = ALLREDUCE, nbytes: int = 0, n_chunks: int = 64,
-                 policy: int = THEMIS, intra: int = SCF, threshold_div: int = 16, charge_latency: bool = False):
+                 policy: int = THEMIS, intra: int = SCF, threshold_div: int = 16, charge_latency: bool = False,
+                 rs_orders=None, ag_orders=None):
+        """rs_orders / ag_orders (C x D, 0-based): caller-given per-chunk
+        orders (themis_plan_custom) instead of Algorithm 1."""
         self.topo = topo
         self.coll = coll
         self.nbytes = int(nbytes)
         self.n_chunks = n_chunks
         self.policy = policy
         self.intra = intra
-        self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency)
+        if rs_orders is None and ag_orders is None:
+            self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency)
+        else:
+            req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency))
+            rs = None if rs_orders is None else np.ascontiguousarray(np.asarray(rs_orders, np.uint8).reshape(-1))
+            ag = None if ag_orders is None else np.ascontiguousarray(np.asarray(ag_orders, np.uint8).reshape(-1))
+            out = C.c_void_p()
+            tc = topo.to_c()
+            check(lib().themis_plan_custom(C.byref(tc), C.byref(req), None if rs is None else rs.ctypes.data,
+                                           None if ag is None else ag.ctypes.data, C.byref(out)))
+            self.h = out
         self.comm = None
         i = PlanInfo_t()
         check(lib().themis_plan_info(self.h, C.byref(i)))

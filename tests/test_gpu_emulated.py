@@ -157,6 +157,39 @@ def test_ring_needs_tma_engine():
     assert e.value.status == 1
 
 
+@pytest.mark.parametrize("sizes", [(2, 2, 2), (4, 2), (3, 2, 2)])
+def test_custom_orders_non_reversed_ag(sizes):
+    """Any RS order x any AG order per chunk (PAPER.md:420-430 Observation 1:
+    the AG order may differ from the RS order) executes correctly."""
+    import itertools
+    import random
+    from fractions import Fraction
+    rng = random.Random(len(sizes) * 7 + sizes[0])
+    D, P, C = len(sizes), int(np.prod(sizes)), 8
+    perms = list(itertools.permutations(range(D)))
+    rs = [rng.choice(perms) for _ in range(C)]
+    ag = [rng.choice(perms) for _ in range(C)]
+    topo = th.Topology(tuple(sizes), (1,) * D)
+    for dtype, slice_elems in (("i32", 2052), ("f32", 4100)):
+        N = P * C * slice_elems
+        comm = th.Comm(topo, N * 4)
+        comm.set_timeout(10.0)
+        plan = th.Plan(topo, th.ALLREDUCE, N * 4, C, rs_orders=rs, ag_orders=ag).bind(comm, [4] * D)
+        xs = host_inputs(P, N, dtype, dist="wide")
+        for r in range(P):
+            comm.rank_view(r, N, dtype).copy_(torch.from_numpy(xs[r]).cuda())
+        th.run(th.ALLREDUCE, comm, plan, N, dtype)
+        torch.cuda.synchronize()
+        comm.status()
+        o = T.Topology.make(sizes, (1,) * D)
+        sched = S.Schedule(o, S.AR, Fraction(N * 4), C, [S.ChunkSchedule(c, rs[c], ag[c]) for c in range(C)], [], 0)
+        want = O.run_schedule(xs, sched, dtype)
+        for r in range(P):
+            assert np.array_equal(comm.rank_view(r, N, dtype).cpu().numpy(), want[r]), f"rank {r}"
+        plan.close()
+        comm.close()
+
+
 def test_allreduce_ldg_engine():
     check_ar((2, 2, 2), (1, 1, 1), "f32", 8, RAGGED["f32"], engine="ldg")
     check_ar((4, 2), (1, 1), "bf16", 4, RAGGED["bf16"], engine="ldg")

@@ -127,6 +127,41 @@ def test_random_configs():
     assert skipped < 40
 
 
+def test_custom_orders_full_space():
+    """themis_plan_custom: arbitrary RS x AG orders per chunk
+    pre-simulated bit-exactly like the oracle's engine."""
+    import itertools
+    rng = random.Random(99)
+    for _ in range(60):
+        D = rng.randint(1, 3)
+        sizes = [rng.choice([2, 3, 4]) for _ in range(D)]
+        bw = [rng.choice(BWS) for _ in range(D)]
+        o, g = make_pair(sizes, bw)
+        C = rng.randint(1, 12)
+        coll = rng.choice([S.AR, "RS", "AG"])
+        perms = list(itertools.permutations(range(D)))
+        rs = [rng.choice(perms) for _ in range(C)]
+        ag = [rng.choice(perms) for _ in range(C)]
+        chunks = [S.ChunkSchedule(c, rs[c] if coll != "AG" else (), ag[c] if coll != "RS" else ())
+                  for c in range(C)]
+        nbytes = rng.randint(1, 1 << 20) * 4096
+        sched = S.Schedule(o, coll, Fraction(nbytes), C, chunks, [], 0)
+        intra = rng.choice([E.SCF, E.FIFO])
+        m = E.simulate(sched, intra)
+        plan = th.Plan(g, COLLS[coll], nbytes, C, th.THEMIS, INTRA[intra],
+                       rs_orders=rs if coll != "AG" else None, ag_orders=ag if coll != "RS" else None)
+        try:
+            ts = plan.info["time_scale"]
+            assert plan.dim_ops() == [list(x) for x in m.dim_order]
+            assert Fraction(plan.info["makespan"], ts) == m.makespan
+            assert [Fraction(v, plan.info["byte_scale"]) for v in plan.info["dim_volume"]] == m.volume
+        finally:
+            plan.close()
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 4096, 2, rs_orders=[(0, 0), (0, 1)],
+                ag_orders=[(1, 0), (1, 0)])
+
+
 def test_plan_validation_errors():
     with pytest.raises(th.ThemisError) as e:
         th.Plan(th.Topology((1, 4), (1, 1)), th.ALLREDUCE, 1024, 4)
