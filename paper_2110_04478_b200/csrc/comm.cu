@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -80,6 +81,7 @@ struct themis_comm {
   bool trace_on = false;
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
+  double min_cta_bytes = 256.0 * 1024;  // op window sizing (themis_comm_set_min_cta_bytes)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -193,6 +195,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   }
   if (const char* env = getenv("THEMIS_COPY_ENGINE")) c->engine = std::string(env) == "ldg" ? 0 : 1;
   if (const char* env = getenv("THEMIS_STAGES")) c->stages = std::max(1, std::min(kStages, atoi(env)));
+  if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(1.0, atof(env));
   c->max_blocks = nb * c->num_sms;
   *out = c;
   return THEMIS_OK;
@@ -216,6 +219,11 @@ extern "C" themis_status_t themis_comm_status(themis_comm_t* c) {
 extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engine) {
   if (!c || engine < 0 || engine > 1) return fail(THEMIS_ERR_INVALID_ARG, "engine must be 0 (LDG) or 1 (TMA)");
   c->engine = engine;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint64_t bytes) {
+  if (!c || bytes == 0) return fail(THEMIS_ERR_INVALID_ARG, "min_cta_bytes must be > 0");
+  c->min_cta_bytes = (double)bytes;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_stages(themis_comm_t* c, int32_t stages) {
@@ -332,6 +340,28 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     }
   for (int k = 0; k < D; ++k)
     if (n[k] > kMaxCtas) return fail(THEMIS_ERR_INVALID_ARG, "at most 160 CTAs per dimension group");
+  // Op windows: an op that moves little gets only as many
+  // CTAs as it can keep busy (>= min_cta_bytes each), and consecutive ops of a
+  // dimension take consecutive CTA windows, so several small chunks' ops of a
+  // dimension run concurrently.  Identical on every GPU (same plan, V, caps).
+  {
+    const double slice = (double)pl->req.bytes / ((double)pl->P * pl->C);
+    const double min_b = c->min_cta_bytes;
+    for (int k = 0; k < D; ++k) {
+      int off = 0;
+      for (size_t i = 0; i < pl->dim_ops[k].size(); ++i) {
+        const uint32_t e = pl->dim_ops[k][i];
+        OpDesc& d = ops[(e >> 8) * pl->NS + (e & 0xFF)];
+        const double mult = (d.phase == 1 && !d.ring) ? (double)(pl->topo.size[k] - 1) : 1.0;
+        const double work = (double)c->V * (double)d.nblk * slice * mult;
+        int w = (int)std::ceil(work / min_b);
+        w = std::max(1, std::min(n[k], w));
+        d.width = w;
+        d.offset = off;
+        off = (off + w) % n[k];
+      }
+    }
+  }
   free_bind(pl);
   auto* b = new BindState();
   b->comm = c;

@@ -28,6 +28,7 @@ struct OpDesc {
   int32_t next_dim;                  // dim of stage+1 (-1: last stage)
   int32_t ring;                      // 1: ring algorithm on this dim
   int32_t seq;                       // index of the op in its dim's enforced list
+  int32_t width, offset;             // the op runs on CTAs [offset, offset+width) mod c_k of its group
   int32_t nfree;                     // dims whose block digit is free
   int32_t free_size[THEMIS_MAX_DIMS];
   int64_t free_stride[THEMIS_MAX_DIMS];
@@ -133,6 +134,16 @@ struct Item {
   int j;          // direct AG: source member
   uint64_t off;   // byte offset of the slice inside a rank's data region
 };
+
+// Small ops run on a window of `width` CTAs so that several chunks' ops of the
+// same dimension are in flight at once ("multiple chunks
+// per dimension should be run in parallel" when one cannot saturate the BW).
+// li = CTA index inside the window, wn = window width.
+__device__ __forceinline__ bool op_member(const OpDesc& d, int gi, int gn, int& li, int& wn) {
+  li = (gi - d.offset + gn) % gn;
+  wn = d.width;
+  return li < wn;
+}
 
 __device__ __forceinline__ int unit_mode(const OpDesc& d) {
   return d.ring ? (d.phase == 0 ? U_RING_RS : U_RING_AG) : (d.phase == 0 ? U_DIRECT_RS : U_DIRECT_AG);
@@ -472,25 +483,27 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
-        if (!unit_has_work(p, d, mode, gi, gn)) continue;  // nothing to wait for or move
+        int li, wn;
+        if (!op_member(d, gi, gn, li, wn)) continue;          // op runs on other CTAs of the group
+        if (!unit_has_work(p, d, mode, li, wn)) continue;     // nothing to wait for or move
         uint64_t t_op = 0;
         double sent = 0.0;
         bool stop = false;
         for (int u = 0; u < nu && !stop; ++u) {
-          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
+          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, li)) {
             stop = true;
             break;
           }
           if (lane == 0) {
             if (u == 0) {
-              if (p.trace && gi == 0) p.trace[2 * opi] = dev::globaltimer();
+              if (p.trace && li == 0) p.trace[2 * opi] = dev::globaltimer();
               if (p.pace_ns_per_byte[d.dim] > 0.f) {  // group-shared pacing origin (first starter wins)
                 const unsigned long long now = dev::globaltimer();
                 const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
                 t_op = prev ? prev : now;
               }
             }
-            produce_unit(p, d, mode, u, gi, gn, smem, full, empty, ctr, t_op, sent);
+            produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent);
           }
           __syncwarp();
         }
@@ -507,8 +520,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
+        int li, wn;
+        if (!op_member(d, gi, gn, li, wn)) continue;
         for (int u = 0; u < nu; ++u, ++n) {
-          if (!consume_unit<Tag>(p, d, mode, u, gi, gn, smem, full, empty, ctr)) {
+          if (!consume_unit<Tag>(p, d, mode, u, li, wn, smem, full, empty, ctr)) {
             run = false;
             break;
           }
@@ -535,7 +550,9 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
-        const bool work = unit_has_work(p, d, mode, gi, gn);
+        int li, wn;
+        if (!op_member(d, gi, gn, li, wn)) continue;
+        const bool work = unit_has_work(p, d, mode, li, wn);
         for (int u = 0; u < nu; ++u, ++n) {
           const int slot = n % kOpRing;
           bool w = true;
@@ -545,9 +562,9 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
             break;
           }
           if (u + 1 < nu) {
-            if (work) publish_ring_warp(p, d, u, gi);
+            if (work) publish_ring_warp(p, d, u, li);
           } else {
-            complete_op_warp(p, d, opi, gn);
+            complete_op_warp(p, d, opi, wn);
           }
           if (lane == 0) dev::mbar_arrive(&op_free[slot]);
         }
@@ -558,6 +575,8 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       const int opi = list[i];
       const OpDesc& d = p.ops[opi];
       const int k = d.dim;
+      int li, wn;
+      if (!op_member(d, gi, gn, li, wn)) continue;
       if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
         const int pk = p.size[k];
         for (int t = tid; t < V * pk; t += blockDim.x) {
@@ -568,10 +587,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         ok = __syncthreads_and(ok);
         if (!ok) break;
       }
-      if (p.trace && gi == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
-      run_op_ldg<Tag>(p, d, gi, gn);
+      if (p.trace && li == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
+      run_op_ldg<Tag>(p, d, li, wn);
       __syncthreads();
-      if (warp == 0) complete_op_warp(p, d, opi, gn);
+      if (warp == 0) complete_op_warp(p, d, opi, wn);
       __syncthreads();
     }
   }

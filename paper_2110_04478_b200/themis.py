@@ -246,6 +246,10 @@ class Comm:
         """TMA ring depth per CTA (bytes in flight = stages x 32 KiB)."""
         check(lib().themis_comm_set_stages(self.h, int(stages)))
 
+    def set_min_cta_bytes(self, nbytes: int) -> None:
+        """Op-window sizing: small ops run on fewer CTAs, several in flight."""
+        check(lib().themis_comm_set_min_cta_bytes(self.h, int(nbytes)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
 

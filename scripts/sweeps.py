@@ -190,6 +190,7 @@ def main():
     ap.add_argument("--config", type=int, required=True, choices=[3, 4, 5])
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     torch.cuda.set_device(local)
     r = Runner(group, rank, world, local)
