@@ -194,8 +194,9 @@ themis_status_t themis_comm_set_stages(themis_comm_t* comm, int32_t stages);
 /* Op windows (PAPER.md:461, :491 — several chunks per dimension in flight when
  * one chunk cannot saturate it): at bind, an op whose bytes on this GPU are
  * below c_k * min_cta_bytes runs on ceil(bytes / min_cta_bytes) CTAs of its
- * dimension group, consecutive ops taking consecutive windows.  Default
- * 256 KiB (env THEMIS_MIN_CTA_BYTES); takes effect at the next
+ * dimension group, consecutive ops taking consecutive windows.  0 (default,
+ * env THEMIS_MIN_CTA_BYTES) = every op on all c_k CTAs, one op at a time per
+ * dimension as in the pre-simulation.  Takes effect at the next
  * themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t bytes);
 /* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */

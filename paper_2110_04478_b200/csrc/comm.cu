@@ -81,7 +81,7 @@ struct themis_comm {
   bool trace_on = false;
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
-  double min_cta_bytes = 256.0 * 1024;  // op window sizing (themis_comm_set_min_cta_bytes)
+  double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -195,7 +195,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   }
   if (const char* env = getenv("THEMIS_COPY_ENGINE")) c->engine = std::string(env) == "ldg" ? 0 : 1;
   if (const char* env = getenv("THEMIS_STAGES")) c->stages = std::max(1, std::min(kStages, atoi(env)));
-  if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(1.0, atof(env));
+  if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   c->max_blocks = nb * c->num_sms;
   *out = c;
   return THEMIS_OK;
@@ -222,7 +222,7 @@ extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engi
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint64_t bytes) {
-  if (!c || bytes == 0) return fail(THEMIS_ERR_INVALID_ARG, "min_cta_bytes must be > 0");
+  if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
   c->min_cta_bytes = (double)bytes;
   return THEMIS_OK;
 }
@@ -354,7 +354,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
         OpDesc& d = ops[(e >> 8) * pl->NS + (e & 0xFF)];
         const double mult = (d.phase == 1 && !d.ring) ? (double)(pl->topo.size[k] - 1) : 1.0;
         const double work = (double)c->V * (double)d.nblk * slice * mult;
-        int w = (int)std::ceil(work / min_b);
+        int w = min_b > 0 ? (int)std::ceil(work / min_b) : n[k];
         w = std::max(1, std::min(n[k], w));
         d.width = w;
         d.offset = off;

@@ -490,7 +490,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         double sent = 0.0;
         bool stop = false;
         for (int u = 0; u < nu && !stop; ++u) {
-          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, li)) {
+          // ring step flags are per absolute CTA index gi: each CTA's slot then
+          // sees its ops in order (monotone), and CTA gi of the left neighbour
+          // has the same window index li for this op (identical windows).
+          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
             stop = true;
             break;
           }
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
             break;
           }
           if (u + 1 < nu) {
-            if (work) publish_ring_warp(p, d, u, li);
+            if (work) publish_ring_warp(p, d, u, gi);
           } else {
             complete_op_warp(p, d, opi, wn);
           }

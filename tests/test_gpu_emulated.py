@@ -41,7 +41,7 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
-             intra=th.SCF, repeat=1, kinds=None, dist="recipe"):
+             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
@@ -49,6 +49,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm = th.Comm(topo, N * esz)
     comm.set_engine(engine)
     comm.set_timeout(10.0)
+    comm.set_min_cta_bytes(min_cta_bytes)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra).bind(comm, ctas)
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
@@ -134,6 +135,16 @@ def test_ring_dimensions(sizes, kinds):
     check_ar(sizes, bw, "i32", 4, 2052, kinds=kinds)
     check_ar(sizes, bw, "f32", 4, RAGGED["f32"], kinds=kinds, dist="wide")
     check_ar(sizes, bw, "f32", 2, 4100, kinds=kinds, dist="wide", ctas=[3] * len(sizes))
+
+
+@pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), (Dk, Dk, Dk)), ((4, 2), (R, Dk)), ((3, 2, 2), (R, Dk, R))])
+def test_op_windows_several_ops_in_flight(sizes, kinds):
+    """Op windows: small ops on CTA windows, several ops of
+    a dimension in flight — results unchanged (int32 exact, f32 bit-exact)."""
+    bw = (1,) * len(sizes)
+    for mcb in (4096, 65536):
+        check_ar(sizes, bw, "i32", 64, 516, kinds=kinds, min_cta_bytes=mcb, ctas=[12] * len(sizes))
+        check_ar(sizes, bw, "f32", 16, 2052, kinds=kinds, min_cta_bytes=mcb, dist="wide")
 
 
 def test_ring_reduce_scatter_all_gather():
@@ -306,6 +317,7 @@ def test_trace_follows_enforced_order():
     N = 8 * C_ * 4096
     comm = th.Comm(topo, N * 4)
     comm.enable_trace(True)
+    comm.set_min_cta_bytes(0)   # full-width ops: one op at a time per dim group
     plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm, [4, 4, 4])
     try:
         th.run(th.ALLREDUCE, comm, plan, N, "f32")
