@@ -206,6 +206,11 @@ themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns
  * out[(chunk*n_stages + stage)*2 + {0,1}] in ns, n = C*n_stages*2 entries. */
 themis_status_t themis_comm_enable_trace(themis_comm_t* comm, int32_t enable);
 themis_status_t themis_trace_fetch(themis_comm_t* comm, uint64_t* out /*[host,out]*/, size_t n);
+/* Trace level 2 (themis_comm_enable_trace(comm, 2)): 6 extra %globaltimer
+ * stamps per op, out[op*6 + j]: 0 producer issued its last tile (window CTA 0),
+ * 1 consumers done (window CTA 0), 2 a CTA's completion warp reached the op
+ * counter, 3 last CTA's atomic returned, 4 after its fence.acq_rel.sys, 5 unused. */
+themis_status_t themis_trace_fetch_detail(themis_comm_t* comm, uint64_t* out /*[host,out]*/, size_t n);
 
 /* Attach a plan to a comm with per-dimension CTA counts.  ctas_per_dim[k] =
  * CTAs (SMs) of dimension k's group; NULL = proportional to bw_mbps over all

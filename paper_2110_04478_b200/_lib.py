@@ -75,6 +75,7 @@ SIGNATURES = {
     "themis_comm_set_timeout": (_ST, [_P, C.c_uint64]),
     "themis_comm_enable_trace": (_ST, [_P, C.c_int32]),
     "themis_trace_fetch": (_ST, [_P, _P, C.c_size_t]),
+    "themis_trace_fetch_detail": (_ST, [_P, _P, C.c_size_t]),
     "themis_plan_bind": (_ST, [_P, _P, _P]),
     "themis_plan_bound_ctas": (_ST, [_P, _P]),
     "themis_allreduce": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),

@@ -78,7 +78,7 @@ struct themis_comm {
   uint32_t* herr_host = nullptr;
   uint32_t* herr_dev = nullptr;
   uint64_t* trace = nullptr;
-  bool trace_on = false;
+  int trace_on = 0;  // 1: per-op start/end, 2: + detailed stamps
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
@@ -176,8 +176,8 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
       (e = cudaMalloc(&c->op_t0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->op_t0, 0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->opcnt, 0, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
-      (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 2 * kMaxOps)) != cudaSuccess ||
-      (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 2 * kMaxOps)) != cudaSuccess ||
+      (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
+      (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
       (e = cudaHostAlloc(&c->herr_host, sizeof(uint32_t), cudaHostAllocMapped)) != cudaSuccess ||
       (e = cudaHostGetDevicePointer(&c->herr_dev, c->herr_host, 0)) != cudaSuccess) {
     delete c;
@@ -243,12 +243,17 @@ extern "C" themis_status_t themis_comm_set_timeout(themis_comm_t* c, uint64_t ns
 }
 extern "C" themis_status_t themis_comm_enable_trace(themis_comm_t* c, int32_t on) {
   if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
-  c->trace_on = on != 0;
+  c->trace_on = on < 0 ? 0 : (on > 2 ? 2 : on);
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_trace_fetch(themis_comm_t* c, uint64_t* out, size_t n) {
   if (!c || !out || n > 2ull * kMaxOps) return fail(THEMIS_ERR_INVALID_ARG, "bad trace args");
   CUDA_TRY(cudaMemcpy(out, c->trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_trace_fetch_detail(themis_comm_t* c, uint64_t* out, size_t n) {
+  if (!c || !out || n > 6ull * kMaxOps) return fail(THEMIS_ERR_INVALID_ARG, "bad trace args");
+  CUDA_TRY(cudaMemcpy(out, c->trace + 2 * kMaxOps, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return THEMIS_OK;
 }
 
@@ -449,6 +454,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.herr = c->herr_dev;
   kp.timeout_ns = c->timeout_ns;
   kp.trace = c->trace_on ? c->trace : nullptr;
+  kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   kp.stages = c->stages;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =

@@ -57,6 +57,7 @@ struct KParams {
   uint32_t* herr;           // host-mapped error word
   uint64_t timeout_ns;
   uint64_t* trace;          // [C*NS*2] or null
+  uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
   int32_t stages;           // TMA ring depth in use (<= kStages): bytes in flight per CTA
 };
@@ -414,11 +415,14 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
   const int lane = threadIdx.x & 31;
   uint32_t last = 0;
   if (lane == 0) {
+    if (p.tdetail) p.tdetail[6 * opi + 2] = dev::globaltimer();  // (any CTA; last writer wins)
     last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
     if (last) {
+      if (p.tdetail) p.tdetail[6 * opi + 3] = dev::globaltimer();
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
       p.op_t0[opi] = 0;
       dev::fence_acq_rel_sys();
+      if (p.tdetail) p.tdetail[6 * opi + 4] = dev::globaltimer();
     }
   }
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
@@ -507,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
               }
             }
             produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent);
+            if (p.tdetail && li == 0 && u + 1 == nu) p.tdetail[6 * opi + 0] = dev::globaltimer();
           }
           __syncwarp();
         }
@@ -533,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           __syncwarp();
           bool w = true;
           if (lane == 0) {
+            if (p.tdetail && li == 0 && warp == 1 && u + 1 == nu) p.tdetail[6 * opi + 1] = dev::globaltimer();
             const int slot = n % kOpRing;
             w = dev::mbar_wait_or(&op_free[slot], ((n / kOpRing) & 1) ^ 1, p.abort_flag);
             if (w) dev::mbar_arrive(&op_done[slot]);

@@ -253,8 +253,15 @@ class Comm:
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
 
-    def enable_trace(self, on: bool = True) -> None:
+    def enable_trace(self, on=True) -> None:
+        """on: False/0 off, True/1 per-op start/end, 2 detailed stamps."""
         check(lib().themis_comm_enable_trace(self.h, int(on)))
+
+    def fetch_trace_detail(self, plan: "Plan") -> np.ndarray:
+        n = plan.info["n_chunks"] * plan.info["n_stages"] * 6
+        out = np.zeros(n, np.uint64)
+        check(lib().themis_trace_fetch_detail(self.h, out.ctypes.data, n))
+        return out.reshape(plan.info["n_chunks"], plan.info["n_stages"], 6)
 
     def fetch_trace(self, plan: Plan) -> np.ndarray:
         n = plan.info["n_chunks"] * plan.info["n_stages"] * 2
