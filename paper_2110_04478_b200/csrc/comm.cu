@@ -213,6 +213,9 @@ extern "C" void themis_comm_free(themis_comm_t* c) {
 extern "C" themis_status_t themis_comm_status(themis_comm_t* c) {
   if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
   uint32_t v = *(volatile uint32_t*)c->herr_host;
+  if ((v & 0xFF) == THEMIS_ERR_PLAN_MISMATCH)
+    return fail(THEMIS_ERR_PLAN_MISMATCH, "rank " + std::to_string(v >> 8) +
+                                              " launched a different plan / count / dtype / CTA caps (plan hash differs)");
   if (v) return fail((themis_status_t)(v & 0xFF), "device watchdog fired while waiting (code " + std::to_string(v >> 8) + ")");
   return THEMIS_OK;
 }
@@ -455,6 +458,13 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.timeout_ns = c->timeout_ns;
   kp.trace = c->trace_on ? c->trace : nullptr;
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
+  // the plan hash covers the inputs, schedule and per-dim order; mix in the
+  // bound CTA caps and the byte count so every rank must launch identically
+  {
+    uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
+    for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
+    kp.plan_hash = h;
+  }
   kp.stages = c->stages;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =

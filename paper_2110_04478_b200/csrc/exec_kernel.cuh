@@ -50,6 +50,7 @@ struct KParams {
   uint64_t slice_elems;     // N / (P*C)
   int32_t elem_size;
   uint32_t epoch;
+  unsigned long long plan_hash;  // must be identical on every rank (checked at entry)
   uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
   unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
   uint32_t* done_cnt;
@@ -65,9 +66,10 @@ struct KParams {
 // ---------------------------------------------------------------- signal pads
 // pad(q) = [entry u32 P][exit u32 P][ready u32 P x kMaxOps][ring u64 P x 8 x kMaxCtas]
 __host__ __device__ __forceinline__ uint64_t ring_flags_offset(int P) { return 4ull * (2ull * P + (uint64_t)P * kMaxOps); }
-__host__ __device__ __forceinline__ uint64_t pad_bytes(int P) {
+__host__ __device__ __forceinline__ uint64_t hash_offset(int P) {
   return ring_flags_offset(P) + 8ull * P * THEMIS_MAX_DIMS * kMaxCtas;
 }
+__host__ __device__ __forceinline__ uint64_t pad_bytes(int P) { return hash_offset(P) + 8ull * P; }
 __device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
   return reinterpret_cast<uint32_t*>(p.heap[q / p.V] + (uint64_t)(q % p.V) * p.sig_bytes);
 }
@@ -80,6 +82,10 @@ __device__ __forceinline__ uint32_t* ready_slot(const KParams& p, int q, int src
 __device__ __forceinline__ unsigned long long* ring_slot(const KParams& p, int q, int src, int k, int g) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig_of(p, q)) + ring_flags_offset(p.P)) +
          ((uint64_t)src * THEMIS_MAX_DIMS + k) * kMaxCtas + g;
+}
+// plan hash announced by rank `src` for the current call, in q's pad
+__device__ __forceinline__ unsigned long long* hash_slot(const KParams& p, int q, int src) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig_of(p, q)) + hash_offset(p.P)) + src;
 }
 __device__ __forceinline__ char* data_of(const KParams& p, int q) {
   return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
@@ -466,11 +472,24 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     dev::fence_mbar_init();
   }
 
-  // a6: entry barrier — every local rank announces the epoch to every rank.
+  // a6: entry barrier — every local rank announces the epoch (and, ordered
+  // before it by the release, its plan hash) to every rank.  Inter-dimension
+  // schedule consistency: every CTA checks that all ranks
+  // run the identical plan; a mismatch latches THEMIS_ERR_PLAN_MISMATCH.
   if (blockIdx.x == 0)
-    for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), p.epoch);
-  for (int i = tid; i < V * P; i += blockDim.x)
+    for (int i = tid; i < V * P; i += blockDim.x) {
+      dev::st_relaxed_sys64(hash_slot(p, i % P, q0 + i / P), p.plan_hash);
+      dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), p.epoch);
+    }
+  for (int i = tid; i < V * P; i += blockDim.x) {
     ok &= wait_geq(p, entry_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFFu);
+    if (ok && *(volatile unsigned long long*)hash_slot(p, q0 + i / P, i % P) != p.plan_hash) {
+      ok = false;
+      atomicExch(p.abort_flag, 1u);
+      *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_PLAN_MISMATCH | ((uint32_t)(i % P) << 8);
+      __threadfence_system();
+    }
+  }
   ok = __syncthreads_and(ok);
 
   // a9: walk this dimension's ops in the enforced order.

@@ -61,6 +61,27 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, ki
     return bad
 
 
+def fault_case(group, W, g):
+    """Fault injection: rank 1 launches a plan
+    with a different intra-dimension policy.  Every rank must report
+    THEMIS_ERR_PLAN_MISMATCH (in-kernel plan-hash check) instead of hanging."""
+    topo = th.Topology((W,), (1,))
+    N = W * 4 * 1024
+    comm = th.Comm(topo, N * 4, group=group)
+    comm.set_timeout(10.0)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, 4, th.THEMIS, th.FIFO if g == 1 else th.SCF).bind(comm)
+    th.run(th.ALLREDUCE, comm, plan, N, "f32")
+    torch.cuda.synchronize()
+    try:
+        comm.status()
+        status = 0
+    except th.ThemisError as e:
+        status = e.status
+    plan.close()
+    comm.close()
+    return status
+
+
 def main():
     rank, W, local, group = init_from_env("nccl")
     cases = []
@@ -86,6 +107,9 @@ def main():
         if bad:
             fails.append((c, bad))
     import torch.distributed as dist
+    st = fault_case(group, W, rank)
+    if st != 6:
+        fails.append((("fault-injection plan mismatch",), [f"status {st}"]))
     t = torch.tensor([len(fails)], device="cuda")
     dist.all_reduce(t)
     if rank == 0:
