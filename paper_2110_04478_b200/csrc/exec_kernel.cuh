@@ -90,7 +90,10 @@ __device__ __forceinline__ unsigned long long* hash_slot(const KParams& p, int q
 __device__ __forceinline__ char* data_of(const KParams& p, int q) {
   return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
 }
-__device__ __forceinline__ int coord(const KParams& p, int q, int k) { return (int)((q / p.stride[k]) % p.size[k]); }
+// 32-bit arithmetic: a comm hosts <= 64 logical ranks (64-bit division is emulated)
+__device__ __forceinline__ int coord(const KParams& p, int q, int k) {
+  return (q / (int)p.stride[k]) % p.size[k];
+}
 // neighbour of q on dim k at coordinate offset delta (ring left = -1, right = +1)
 __device__ __forceinline__ int ring_peer(const KParams& p, int q, int k, int delta) {
   const int pk = p.size[k], c = coord(p, q, k);
@@ -403,7 +406,15 @@ __device__ __forceinline__ bool wait_ring_warp(const KParams& p, const OpDesc& d
 // One warp: this CTA finished ring step `step` -> tell the right neighbours.
 __device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc& d, int step, int gi) {
   const int V = p.V, q0 = p.my_gpu * V, k = d.dim, lane = threadIdx.x & 31;
-  if (lane == 0) dev::fence_acq_rel_sys();
+  bool local = true;
+  for (int v = lane; v < V; v += 32) local &= ring_peer(p, q0 + v, k, +1) / V == p.my_gpu;
+  local = __all_sync(0xFFFFFFFFu, local);
+  if (lane == 0) {
+    if (local)
+      dev::fence_acq_rel_gpu();
+    else
+      dev::fence_acq_rel_sys();
+  }
   __syncwarp();
   for (int v = lane; v < V; v += 32) {
     const int q = q0 + v;
@@ -427,18 +438,35 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
       if (p.tdetail) p.tdetail[6 * opi + 3] = dev::globaltimer();
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
       p.op_t0[opi] = 0;
-      dev::fence_acq_rel_sys();
-      if (p.tdetail) p.tdetail[6 * opi + 4] = dev::globaltimer();
     }
   }
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
   if (!last) return;
-  if (d.next_dim >= 0) {
+  if (d.next_dim >= 0) {  // (the last stage has no consumer: the exit barrier orders it)
     const int V = p.V, q0 = p.my_gpu * V, kn = d.next_dim, pn = p.size[kn];
+    // The consumers of the flag read the data next.  If all of them are on
+    // this GPU a gpu-scope release suffices; otherwise fence at sys scope.
+    bool local = true;
+    for (int t = lane; t < V * pn; t += 32) {
+      const int q = q0 + t / pn;
+      local &= (q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn]) / V == p.my_gpu;
+    }
+    local = __all_sync(0xFFFFFFFFu, local);
+    if (lane == 0) {
+      if (local)
+        dev::fence_acq_rel_gpu();
+      else
+        dev::fence_acq_rel_sys();
+      if (p.tdetail) p.tdetail[6 * opi + 4] = dev::globaltimer();
+    }
+    __syncwarp();
     for (int t = lane; t < V * pn; t += 32) {
       const int q = q0 + t / pn;
       const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
-      dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
+      if (local)
+        dev::st_relaxed_gpu(ready_slot(p, dst, q, opi), p.epoch);
+      else
+        dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
     }
   }
   if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
