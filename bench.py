@@ -144,7 +144,7 @@ def run_themis(a):
     from paper_2110_04478_b200.dist import barrier, init_from_env, max_over_ranks
     from synth import device_input
 
-    os.environ.setdefault("NCCL_DEBUG", "WARN")      # keep stdout to the one JSON line
+    os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (NCCL prints its version at INFO)
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
@@ -254,6 +254,42 @@ def run_themis(a):
                 compare[f"{mode} {':'.join(map(str, rat))}"] = row
         comm.set_pacing(False)
 
+    # Achieved per-dimension GB/s (north_star (d)): one traced, paced Themis
+    # All-Reduce; busy_K = union of dim K's op intervals (%globaltimer),
+    # achieved_K = N_K / busy_K per rank, against the emulated BW_K.
+    per_dim = None
+    if not a.no_compare:
+        rat = a.compare[0] if a.compare else ratio
+        bw = paced_bw(rat, pace_gbs)
+        comm.set_pacing(True)
+        comm.enable_trace(True)
+        p = make(th.THEMIS, rat, pace_gbs)
+        refill()
+        th.run(th.ALLREDUCE, comm, p, N, "f32")
+        torch.cuda.synchronize()
+        comm.status()
+        tr = comm.fetch_trace(p).astype("int64")
+        per_dim = {"ratio": ":".join(map(str, rat)), "dims": []}
+        for k, ops in enumerate(p.dim_ops()):
+            iv = sorted((int(tr[c, s, 0]), int(tr[c, s, 1])) for c, s in ops)
+            busy, cs, ce = 0, iv[0][0], iv[0][1]
+            for s0, e0 in iv[1:]:
+                if s0 > ce:
+                    busy += ce - cs
+                    cs, ce = s0, e0
+                else:
+                    ce = max(ce, e0)
+            busy += ce - cs
+            nk = p.info["dim_volume"][k] / p.info["byte_scale"]
+            per_dim["dims"].append({"dim": k + 1, "emulated_gbs": bw[k] / 1000, "bytes_per_rank": nk,
+                                    "busy_us": round(busy / 1e3, 1),
+                                    "achieved_gbs": round(nk / busy, 2) if busy else None})
+        span = int(tr[:, :, 1].max() - tr[:, :, 0].min())
+        per_dim["span_us"] = round(span / 1e3, 1)
+        p.close()
+        comm.enable_trace(False)
+        comm.set_pacing(False)
+
     # NCCL all_reduce on the same bytes (context row, N > 1 only)
     nccl = None
     if world > 1 and not a.no_compare:
@@ -348,9 +384,9 @@ def run_themis(a):
                        "l2": "inputs refreshed from a pristine copy before every step (>= 1 GiB per GPU written, "
                              "> 126 MB L2); inputs larger than L2"},
             "clocks": clocks.summary(), "gpu_launches": launches, "roofline": roof, "e2e": e2e,
-            "compare": compare, "nccl_context": nccl, "cpu_baseline": cpu,
+            "compare": compare, "per_dim_emulation": per_dim, "nccl_context": nccl, "cpu_baseline": cpu,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     main.close()
     comm.close()
     if world > 1:
@@ -410,10 +446,24 @@ def run_reference(a):
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
                             "sample": f"{a.cpu_mib} MiB fp32 per rank x {P} simulated ranks per step"},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+_JSON_FD = None
+
+
+def emit(obj) -> None:
+    """Write the one JSON result line to the real stdout (fd saved at start;
+    everything else, e.g. NCCL's version banner, goes to stderr)."""
+    line = (json.dumps(obj) + "\n").encode()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, line)
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
