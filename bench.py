@@ -164,14 +164,16 @@ def run_themis(a):
         total_ctas = a.ctas_total
     elif ncross_ == 0:
         total_ctas = sms
-    elif ncross_ == len(SIZES):
-        total_ctas = 32
+    elif ncross_ == len(SIZES):   # every dim over NVLink: ~16 CTAs per dim group + 16
+        total_ctas = min(sms, 16 * len(SIZES) + 16)
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
     stages = a.stages or (6 if ncross_ == 0 else 4)
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
     comm.set_timeout(30.0)
+    comm.set_stages(1)
+    comm.set_stage_bytes(a.stage_kb * 1024)
     comm.set_stages(stages)
     pristine = [device_input(rank * V + v, N, "f32", dev) for v in range(V)]
 
@@ -479,6 +481,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
+    ap.add_argument("--stage-kb", type=int, default=32, help="TMA ring stage size (KiB)")
     ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")
     ap.add_argument("--compare-ratios", default="", help="extra emulated ratios, e.g. '1:1:1,2:2:1'")
     a = ap.parse_args()

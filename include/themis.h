@@ -188,9 +188,12 @@ themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
  * per-rank rate is capped at the bound plan topology's absolute bw_mbps[k]
  * (B_K = 1/BW_K).  Off (default): only the CTA caps limit it. */
 themis_status_t themis_comm_set_pacing(themis_comm_t* comm, int32_t on);
-/* TMA ring depth per CTA, 1..6 stages of 32 KiB (bytes in flight per CTA);
- * default 6, env THEMIS_STAGES.  Errors: INVALID_ARG. */
+/* TMA ring per CTA: `stages` slots of `stage_bytes` (bytes in flight per CTA
+ * = stages x stage_bytes <= 192 KiB); defaults 6 x 32 KiB, env THEMIS_STAGES /
+ * THEMIS_STAGE_KB.  A tile moves stage_bytes / n_sources bytes per source.
+ * Errors: INVALID_ARG (product too large, stage_bytes < 8 KiB or not KiB-aligned). */
 themis_status_t themis_comm_set_stages(themis_comm_t* comm, int32_t stages);
+themis_status_t themis_comm_set_stage_bytes(themis_comm_t* comm, int32_t stage_bytes);
 /* Op windows (PAPER.md:461, :491 — several chunks per dimension in flight when
  * one chunk cannot saturate it): at bind, an op whose bytes on this GPU are
  * below c_k * min_cta_bytes runs on ceil(bytes / min_cta_bytes) CTAs of its

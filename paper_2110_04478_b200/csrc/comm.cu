@@ -81,6 +81,7 @@ struct themis_comm {
   int trace_on = 0;  // 1: per-op start/end, 2: + detailed stamps
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
+  int stage_bytes = kStageBytes;  // bytes per ring stage (themis_comm_set_stage_bytes)
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
@@ -194,7 +195,10 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     return cuda_fail(e, "kernel attributes / occupancy query");
   }
   if (const char* env = getenv("THEMIS_COPY_ENGINE")) c->engine = std::string(env) == "ldg" ? 0 : 1;
-  if (const char* env = getenv("THEMIS_STAGES")) c->stages = std::max(1, std::min(kStages, atoi(env)));
+  if (const char* env = getenv("THEMIS_STAGE_KB"))
+    c->stage_bytes = std::max(8, std::min(3 * kStageBytes / 1024, atoi(env))) * 1024;
+  if (const char* env = getenv("THEMIS_STAGES"))
+    c->stages = std::max(1, std::min(kStages * kStageBytes / c->stage_bytes, atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   c->max_blocks = nb * c->num_sms;
   *out = c;
@@ -230,8 +234,15 @@ extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint6
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_stages(themis_comm_t* c, int32_t stages) {
-  if (!c || stages < 1 || stages > kStages) return fail(THEMIS_ERR_INVALID_ARG, "stages must be 1..6");
+  if (!c || stages < 1 || (int64_t)stages * c->stage_bytes > (int64_t)kStages * kStageBytes)
+    return fail(THEMIS_ERR_INVALID_ARG, "stages * stage_bytes must be <= 192 KiB");
   c->stages = stages;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_stage_bytes(themis_comm_t* c, int32_t bytes) {
+  if (!c || bytes < 8192 || bytes % 1024 || (int64_t)bytes * c->stages > (int64_t)kStages * kStageBytes)
+    return fail(THEMIS_ERR_INVALID_ARG, "stage_bytes: multiple of 1 KiB, >= 8 KiB, stages * stage_bytes <= 192 KiB");
+  c->stage_bytes = bytes;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_pacing(themis_comm_t* c, int32_t on) {
@@ -466,6 +477,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
     kp.plan_hash = h;
   }
   kp.stages = c->stages;
+  kp.stage_bytes = c->stage_bytes;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;

@@ -60,7 +60,8 @@ struct KParams {
   uint64_t* trace;          // [C*NS*2] or null
   uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
-  int32_t stages;           // TMA ring depth in use (<= kStages): bytes in flight per CTA
+  int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
+  int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
 };
 
 // ---------------------------------------------------------------- signal pads
@@ -298,14 +299,14 @@ constexpr int kOpRing = 16;  // units the consumers may run ahead of the complet
 constexpr int kSmemBytes = kStages * kStageBytes + 2 * (kStages + kOpRing) * 8;
 static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + completion warp");
 
-__device__ __forceinline__ uint32_t unit_tile(int nsrc) { return ((uint32_t)kStageBytes / nsrc) & ~15u; }
+__device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { return ((uint32_t)p.stage_bytes / nsrc) & ~15u; }
 
 // Producer (one lane): stream this CTA's tiles of one unit into the ring.
 __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
                                              char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
                                              uint64_t t_op, double& sent) {
   const int nsrc = unit_nsrc(p, d, mode);
-  const uint32_t tile = unit_tile(nsrc);
+  const uint32_t tile = unit_tile(p, nsrc);
   const float pace = p.pace_ns_per_byte[d.dim];
   const int remote = mode == U_DIRECT_RS ? p.size[d.dim] - 1 : 1;  // peer sources per tile
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
@@ -325,7 +326,7 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
       const int s = ctr % p.stages;
       dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
       dev::mbar_expect_tx(&full[s], bytes * nsrc);
-      char* dst = smem + s * kStageBytes;
+      char* dst = smem + s * p.stage_bytes;
       for (int j = 0; j < nsrc; ++j) {
         const char* sj = j < 8 ? src[j] : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off;
         dev::bulk_g2s(dst + j * tile, sj + pos, bytes, &full[s]);
@@ -341,7 +342,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
   const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
   constexpr int kCons = 32 * kConsumerWarps;
   const int nsrc = unit_nsrc(p, d, mode);
-  const uint32_t tile = unit_tile(nsrc), tile16 = tile / 16;
+  const uint32_t tile = unit_tile(p, nsrc), tile16 = tile / 16;
   const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
   bool ok = true;
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
@@ -355,7 +356,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         ok = false;
         return;
       }
-      const uint4* sm = reinterpret_cast<const uint4*>(smem + s * kStageBytes);
+      const uint4* sm = reinterpret_cast<const uint4*>(smem + s * p.stage_bytes);
       uint4* dst = reinterpret_cast<uint4*>(base + pos);
       if (reduce) {
         for (uint32_t w = ct; w < n16; w += kCons) {

@@ -243,8 +243,11 @@ class Comm:
         check(lib().themis_comm_set_pacing(self.h, int(on)))
 
     def set_stages(self, stages: int) -> None:
-        """TMA ring depth per CTA (bytes in flight = stages x 32 KiB)."""
+        """TMA ring depth per CTA (bytes in flight = stages x stage_bytes)."""
         check(lib().themis_comm_set_stages(self.h, int(stages)))
+
+    def set_stage_bytes(self, nbytes: int) -> None:
+        check(lib().themis_comm_set_stage_bytes(self.h, int(nbytes)))
 
     def set_min_cta_bytes(self, nbytes: int) -> None:
         """Op-window sizing: small ops run on fewer CTAs, several in flight."""
