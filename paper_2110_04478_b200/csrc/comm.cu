@@ -198,7 +198,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if (const char* env = getenv("THEMIS_STAGE_KB"))
     c->stage_bytes = std::max(8, std::min(3 * kStageBytes / 1024, atoi(env))) * 1024;
   if (const char* env = getenv("THEMIS_STAGES"))
-    c->stages = std::max(1, std::min(kStages * kStageBytes / c->stage_bytes, atoi(env)));
+    c->stages = std::max(1, std::min(std::min(kStages, kStages * kStageBytes / c->stage_bytes), atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   c->max_blocks = nb * c->num_sms;
   *out = c;
@@ -234,8 +234,8 @@ extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint6
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_stages(themis_comm_t* c, int32_t stages) {
-  if (!c || stages < 1 || (int64_t)stages * c->stage_bytes > (int64_t)kStages * kStageBytes)
-    return fail(THEMIS_ERR_INVALID_ARG, "stages * stage_bytes must be <= 192 KiB");
+  if (!c || stages < 1 || stages > kStages || (int64_t)stages * c->stage_bytes > (int64_t)kStages * kStageBytes)
+    return fail(THEMIS_ERR_INVALID_ARG, "stages must be 1..6 with stages * stage_bytes <= 192 KiB");
   c->stages = stages;
   return THEMIS_OK;
 }
