@@ -185,6 +185,52 @@ def run_schedule(inputs, sched: Schedule, dtype: str, order=None):
     return bufs
 
 
+def element_location(topo, N: int, C: int, i: int) -> tuple:
+    """(block b, chunk c) of element i under the layout R16."""
+    blk = N // topo.P
+    b = i // blk
+    c = (i % blk) // (blk // C)
+    return b, c
+
+
+def allreduce_element(vals, topo, rs_order, dtype: str, block: int):
+    """All-Reduce result of ONE element position, computed directly from the
+    stage structure: arrange the P ranks' values of the element on the
+    P_1 x ... x P_D grid and reduce along the chunk's RS dims in `rs_order`,
+    each axis in the dim's summation order (coordinate order; ring dims end at
+    the owner digit of `block`), with the dtype's rounding per stage (R18).
+    AG only copies, so every rank ends with this value.  `vals[r]` is rank r's
+    value (bf16 as uint16 bits).  Used to check full-size runs on samples."""
+    P = topo.P
+    grid = {}
+    for r in range(P):
+        grid[topo.coords(r)] = np.array([vals[r]], dtype=_np_dtype(dtype))
+    live = dict(grid)
+    for k in rs_order:
+        t = digit(topo, block, k)
+        order = summation_order(topo, k, t)
+        nxt = {}
+        for coords, _ in live.items():
+            if coords[k] != 0:
+                continue
+            members = []
+            for j in order:
+                cc = list(coords)
+                cc[k] = j
+                members.append(live[tuple(cc)])
+            out = list(coords)
+            out[k] = t
+            nxt[tuple(out)] = reduce_in_order(members, dtype)
+        # keep only the owner digit along k (the other digits are not held)
+        live = {}
+        for coords, v in nxt.items():
+            for j in range(topo.dims[k].size):
+                cc = list(coords)
+                cc[k] = j
+                live[tuple(cc)] = v
+    return live[topo.coords(block)][0]
+
+
 # --- plain definitions ------------------------------------------------------
 def allreduce_definition(inputs, dtype: str) -> np.ndarray:
     """sum_r x_r: exact int64 sum wrapped mod 2^32 for i32; fp64 otherwise."""

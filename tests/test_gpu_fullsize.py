@@ -1,0 +1,80 @@
+"""Full-size parity (BASELINE.json configs[1]) in the launch configuration
+bench.py times at N = 1: logical 2x2x2 emulated in one GPU, 1 GiB per rank,
+64 chunks, emulated 4:2:1 CTA caps [85, 42, 21], 6 TMA stages.
+
+* sampled elements: bit-exact against the oracle's per-element formulation
+  (oracle.data.allreduce_element, pinned to the step-by-step simulator) with
+  the oracle's own Themis schedule;
+* whole buffer: every rank bitwise identical; fp32 error vs the fp64 sum
+  within 1e-5 * sum|x| (north_star); int32 exact vs the wrapped int64 sum.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import data as O, scheduler as S, topology as T
+from paper_2110_04478_b200 import themis as th
+from synth import device_input
+
+pytestmark = pytest.mark.gpu
+
+SIZES, RATIO, C, MIB = (2, 2, 2), (4, 2, 1), 64, 1024
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "i32"])
+def test_config2_full_size(dtype):
+    topo = th.Topology(SIZES, RATIO)
+    P = topo.P
+    S_ = MIB << 20
+    N = S_ // 4
+    comm = th.Comm(topo, S_)
+    comm.set_stages(6)
+    comm.set_timeout(30.0)
+    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, [85, 42, 21])
+    try:
+        xs = [device_input(r, N, dtype, torch.device("cuda", 0)) for r in range(P)]
+        for r in range(P):
+            comm.rank_view(r, N, dtype).copy_(xs[r])
+        th.run(th.ALLREDUCE, comm, plan, N, dtype)
+        torch.cuda.synchronize()
+        comm.status()
+        outs = [comm.rank_view(r, N, dtype) for r in range(P)]
+        for r in range(1, P):                               # all ranks bitwise identical
+            assert torch.equal(outs[r], outs[0])
+        if dtype == "i32":                                  # exact vs the definition (library sum)
+            s = torch.zeros(N, dtype=torch.int64, device="cuda")
+            for x in xs:
+                s += x.to(torch.int64)
+            want = ((s + 2 ** 31) % 2 ** 32 - 2 ** 31).to(torch.int32)
+            assert torch.equal(outs[0], want)
+        else:                                               # |y - sum| <= 1e-5 sum|x|
+            s = torch.zeros(N, dtype=torch.float64, device="cuda")
+            a = torch.zeros(N, dtype=torch.float64, device="cuda")
+            for x in xs:
+                s += x.to(torch.float64)
+                a += x.to(torch.float64).abs()
+            err = (outs[0].to(torch.float64) - s).abs()
+            assert bool((err <= 1e-5 * a).all())
+            # sampled elements bit-exact vs the oracle, with the oracle's schedule
+            o = T.Topology.make(SIZES, RATIO)
+            sched = S.schedule_collective(o, S.AR, S_, C, S.THEMIS)
+            rng = np.random.default_rng(5)
+            idx = np.unique(np.concatenate([rng.integers(0, N, 1500), [0, N - 1, N // 2, N // P - 1]]))
+            it = torch.from_numpy(idx).cuda()
+            xv = torch.stack([x[it] for x in xs]).cpu().numpy()
+            got = torch.stack([o_[it] for o_ in outs]).cpu().numpy()
+            for n, i in enumerate(idx):
+                b, c = O.element_location(o, N, C, int(i))
+                v = O.allreduce_element(list(xv[:, n]), o, sched.chunks[c].rs, "f32", b)
+                assert np.float32(v).tobytes() == got[0, n].tobytes(), f"element {i}"
+    finally:
+        plan.close()
+        comm.close()
