@@ -164,11 +164,11 @@ def run_themis(a):
         total_ctas = a.ctas_total
     elif ncross_ == 0:
         total_ctas = sms
-    elif ncross_ == len(SIZES):   # every dim over NVLink: ~16 CTAs per dim group + 16
-        total_ctas = min(sms, 16 * len(SIZES) + 16)
+    elif ncross_ == len(SIZES):   # every dim over NVLink (calibration: 2x2 best at 96 CTAs x 3 stages)
+        total_ctas = min(sms, 32 * len(SIZES) + 32) if len(SIZES) > 1 else 32
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
-    stages = a.stages or (6 if ncross_ == 0 else 4)
+    stages = a.stages or (6 if ncross_ == 0 else (3 if ncross_ == len(SIZES) and len(SIZES) > 1 else 4))
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
     comm.set_timeout(30.0)

@@ -54,6 +54,29 @@ if rank == 0:
     print(f"  {'published':20s} median {np.median(rel(tr[:, :, 1])):7.2f} us")
     lat = [tr[c, s, 0] - tr[c, s - 1, 1] for c in range(tr.shape[0]) for s in range(1, tr.shape[1])]
     print(f"  stage transition median {np.median(lat)/1e3:.2f} us p10 {np.percentile(lat, 10)/1e3:.2f}")
+    # per (dim, phase): median op duration and the per-rank bytes it moves -> GB/s
+    rs, ag = plan.orders()
+    D = len(sizes)
+    NS = plan.info["n_stages"]
+    Sb = N * 4 / a.chunks
+    for k in range(D):
+        for ph in ("RS", "AG"):
+            durs, vols = [], []
+            for c in range(a.chunks):
+                order = list(rs[c]) + list(ag[c])
+                h = Sb
+                for s in range(NS):
+                    d = int(order[s])
+                    pk = sizes[d]
+                    is_rs = s < D
+                    v = h * (pk - 1) / pk if is_rs else h * (pk - 1)
+                    if d == k and (ph == "RS") == is_rs:
+                        durs.append(tr[c, s, 1] - tr[c, s, 0])
+                        vols.append(v)
+                    h = h / pk if is_rs else h * pk
+            if durs:
+                print(f"  dim{k+1} {ph}: median op {np.median(durs)/1e3:.1f} us, {np.median(vols)/1e6:.2f} MB/rank "
+                      f"-> {np.median(vols)/np.median(durs):.1f} GB/s per rank")
 plan.close()
 comm.close()
 if group is not None:
