@@ -19,7 +19,7 @@
 // A "unit" is one direct op or one ring step.
 
 constexpr int kMaxCtas = 160;  // CTAs per dimension group (ring step flags)
-enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3 };
+enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3, U_DIRECT_AG_T = 4 };
 
 // Per-op descriptor uploaded at bind (a5).
 struct OpDesc {
@@ -159,9 +159,21 @@ __device__ __forceinline__ bool op_member(const OpDesc& d, int gi, int gn, int& 
 __device__ __forceinline__ int unit_mode(const OpDesc& d) {
   return d.ring ? (d.phase == 0 ? U_RING_RS : U_RING_AG) : (d.phase == 0 ? U_DIRECT_RS : U_DIRECT_AG);
 }
+// TMA path: a direct AG tile pulls the same offsets from all P_k - 1 peers at
+// once (U_DIRECT_AG_T), so every CTA keeps requests in flight to every peer.
+__device__ __forceinline__ int unit_mode_tma(const OpDesc& d) {
+  const int m = unit_mode(d);
+  return m == U_DIRECT_AG ? U_DIRECT_AG_T : m;
+}
 __device__ __forceinline__ uint64_t unit_items(const KParams& p, const OpDesc& d, int mode) {
   return (uint64_t)p.V * d.nblk * (mode == U_DIRECT_AG ? (uint64_t)(p.size[d.dim] - 1) : 1ull);
 }
+// byte distance between the same slice of two parts differing by 1 in digit_k
+__device__ __forceinline__ uint64_t part_stride(const KParams& p, int k) {
+  return (uint64_t)p.stride[k] * p.blk_elems * p.elem_size;
+}
+// the jj-th peer (jj = 0..P_k-2) of a rank with coordinate ck on its dim
+__device__ __forceinline__ int peer_member(int jj, int ck) { return jj < ck ? jj : jj + 1; }
 
 __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, int mode, int step, uint64_t it) {
   Item r;
@@ -182,9 +194,10 @@ __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, i
     f = (int64_t)(it % d.nblk);
     r.j = -1;
     const int ck = coord(p, r.q, k);
-    digit = mode == U_DIRECT_RS ? ck
-          : mode == U_RING_RS   ? (ck + pk - 2 - step) % pk
-                                : ((ck - 1 - step) % pk + pk) % pk;
+    digit = mode == U_DIRECT_RS   ? ck
+          : mode == U_DIRECT_AG_T ? 0  // base: part j is at off + j * part_stride
+          : mode == U_RING_RS     ? (ck + pk - 2 - step) % pk
+                                  : ((ck - 1 - step) % pk + pk) % pk;
   }
   int64_t b = (int64_t)digit * p.stride[k];
   for (int dd = 0; dd < p.D; ++dd)  // other fixed digits: the rank's coords on the reduced dims
@@ -238,13 +251,14 @@ __device__ __forceinline__ bool unit_has_work(const KParams& p, const OpDesc& d,
 
 // sources of a unit's item, in summation order
 __device__ __forceinline__ int unit_nsrc(const KParams& p, const OpDesc& d, int mode) {
-  return mode == U_DIRECT_RS ? p.size[d.dim] : mode == U_RING_RS ? 2 : 1;
+  return mode == U_DIRECT_RS ? p.size[d.dim] : mode == U_DIRECT_AG_T ? p.size[d.dim] - 1 : mode == U_RING_RS ? 2 : 1;
 }
 __device__ __forceinline__ int unit_src_rank(const KParams& p, const OpDesc& d, int mode, const Item& m, int j) {
   const int k = d.dim;
   switch (mode) {
     case U_DIRECT_RS: return m.g0 + j * (int)p.stride[k];
     case U_DIRECT_AG: return m.g0 + m.j * (int)p.stride[k];
+    case U_DIRECT_AG_T: return m.g0 + peer_member(j, coord(p, m.q, k)) * (int)p.stride[k];
     case U_RING_RS: return j == 0 ? ring_peer(p, m.q, k, -1) : m.q;  // left partial + own value
     default: return ring_peer(p, m.q, k, -1);
   }
@@ -308,13 +322,17 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
   const int nsrc = unit_nsrc(p, d, mode);
   const uint32_t tile = unit_tile(p, nsrc);
   const float pace = p.pace_ns_per_byte[d.dim];
-  const int remote = mode == U_DIRECT_RS ? p.size[d.dim] - 1 : 1;  // peer sources per tile
+  const int remote = (mode == U_DIRECT_RS || mode == U_DIRECT_AG_T) ? p.size[d.dim] - 1 : 1;  // peer sources/tile
+  const uint64_t pstride = part_stride(p, d.dim);
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
     const Item m = decode_item(p, d, mode, step, it);
     const char* src[THEMIS_MAX_DIMS > 8 ? THEMIS_MAX_DIMS : 8];
     const int ns = nsrc <= 8 ? nsrc : 8;
-    for (int j = 0; j < ns; ++j) src[j] = data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off;
+    const int ck = coord(p, m.q, d.dim);
+    for (int j = 0; j < ns; ++j)  // AG_T: peer j's own part sits at digit_k = member(j)
+      src[j] = data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off +
+               (mode == U_DIRECT_AG_T ? (uint64_t)peer_member(j, ck) * pstride : 0);
     for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
       const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
       if (pace > 0.f) {  // absolute due times from the group's op origin
@@ -328,7 +346,9 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
       dev::mbar_expect_tx(&full[s], bytes * nsrc);
       char* dst = smem + s * p.stage_bytes;
       for (int j = 0; j < nsrc; ++j) {
-        const char* sj = j < 8 ? src[j] : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off;
+        const char* sj = j < 8 ? src[j]
+                               : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off +
+                                     (mode == U_DIRECT_AG_T ? (uint64_t)peer_member(j, ck) * pstride : 0);
         dev::bulk_g2s(dst + j * tile, sj + pos, bytes, &full[s]);
       }
     }
@@ -364,6 +384,13 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
           Tag::load(acc, sm[w]);
           for (int j = 1; j < nsrc; ++j) Tag::add(acc, sm[j * tile16 + w]);
           dev::st_v4(dst + w, Tag::store(acc));
+        }
+      } else if (mode == U_DIRECT_AG_T) {  // slot j -> peer member(j)'s part
+        const int ck = coord(p, m.q, d.dim);
+        const uint64_t ps16 = part_stride(p, d.dim) / 16;
+        for (int j = 0; j < nsrc; ++j) {
+          uint4* dj = dst + (uint64_t)peer_member(j, ck) * ps16;
+          for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dj + w, sm[j * tile16 + w]);
         }
       } else {
         for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
@@ -533,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       for (int i = 0; i < nops; ++i) {
         const int opi = list[i];
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode(d);
+        const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         if (!op_member(d, gi, gn, li, wn)) continue;          // op runs on other CTAs of the group
@@ -574,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       for (int i = 0; i < nops && run; ++i) {
         const int opi = list[i];
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode(d);
+        const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         if (!op_member(d, gi, gn, li, wn)) continue;
@@ -605,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       for (int i = 0; i < nops && run; ++i) {
         const int opi = list[i];
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode(d);
+        const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         if (!op_member(d, gi, gn, li, wn)) continue;
