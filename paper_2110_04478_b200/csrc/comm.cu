@@ -82,6 +82,7 @@ struct themis_comm {
   bool pacing = false;  // emulate per-dim bandwidth by pacing (themis_comm_set_pacing)
   int stages = kStages;  // TMA ring depth (themis_comm_set_stages)
   int stage_bytes = kStageBytes;  // bytes per ring stage (themis_comm_set_stage_bytes)
+  int ag_rr = 0;                  // direct-AG tile shape (env THEMIS_AG_RR, experiment)
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
@@ -195,6 +196,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     return cuda_fail(e, "kernel attributes / occupancy query");
   }
   if (const char* env = getenv("THEMIS_COPY_ENGINE")) c->engine = std::string(env) == "ldg" ? 0 : 1;
+  if (const char* env = getenv("THEMIS_AG_RR")) c->ag_rr = atoi(env) != 0;
   if (const char* env = getenv("THEMIS_STAGE_KB"))
     c->stage_bytes = std::max(8, std::min(3 * kStageBytes / 1024, atoi(env))) * 1024;
   if (const char* env = getenv("THEMIS_STAGES"))
@@ -478,6 +480,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   }
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;
+  kp.ag_rr = c->ag_rr;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;

@@ -62,6 +62,7 @@ struct KParams {
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
+  int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
 };
 
 // ---------------------------------------------------------------- signal pads
@@ -333,6 +334,30 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
     for (int j = 0; j < ns; ++j)  // AG_T: peer j's own part sits at digit_k = member(j)
       src[j] = data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off +
                (mode == U_DIRECT_AG_T ? (uint64_t)peer_member(j, ck) * pstride : 0);
+    if (mode == U_DIRECT_AG_T && p.ag_rr) {
+      // round-robin variant: each ring stage holds one whole stage_bytes tile
+      // from one peer; consecutive stages cycle through the peers
+      const uint32_t big = p.stage_bytes;
+      for (uint64_t pos = a; pos < e; pos += big) {
+        const uint32_t bytes = (uint32_t)(e - pos < big ? e - pos : big);
+        for (int j = 0; j < nsrc; ++j, ++ctr) {
+          if (pace > 0.f) {
+            const uint64_t due = t_op + (uint64_t)(sent * pace);
+            while (dev::globaltimer() < due) {
+            }
+            sent += (double)bytes;
+          }
+          const int s = ctr % p.stages;
+          dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+          dev::mbar_expect_tx(&full[s], bytes);
+          const char* sj = j < 8 ? src[j]
+                                 : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off +
+                                       (uint64_t)peer_member(j, ck) * pstride;
+          dev::bulk_g2s(smem + s * p.stage_bytes, sj + pos, bytes, &full[s]);
+        }
+      }
+      return;
+    }
     for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
       const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
       if (pace > 0.f) {  // absolute due times from the group's op origin
@@ -369,6 +394,27 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
     if (!ok) return;
     const Item m = decode_item(p, d, mode, step, it);
     char* base = data_of(p, m.q) + m.off;
+    if (mode == U_DIRECT_AG_T && p.ag_rr) {  // mirror of the producer's round-robin stages
+      const uint32_t big = p.stage_bytes;
+      const int ck = coord(p, m.q, d.dim);
+      const uint64_t ps = part_stride(p, d.dim);
+      for (uint64_t pos = a; pos < e; pos += big) {
+        const uint32_t n16 = (uint32_t)((e - pos < big ? e - pos : big) / 16);
+        for (int j = 0; j < nsrc; ++j, ++ctr) {
+          const int s = ctr % p.stages;
+          if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) {
+            ok = false;
+            return;
+          }
+          const uint4* sm = reinterpret_cast<const uint4*>(smem + s * p.stage_bytes);
+          uint4* dj = reinterpret_cast<uint4*>(base + pos + (uint64_t)peer_member(j, ck) * ps);
+          for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dj + w, sm[w]);
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive(&empty[s]);
+        }
+      }
+      return;
+    }
     for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
       const uint32_t n16 = (uint32_t)((e - pos < tile ? e - pos : tile) / 16);
       const int s = ctr % p.stages;
