@@ -1,0 +1,33 @@
+"""CPU checks of bench.py's roofline / emulation arithmetic."""
+
+from fractions import Fraction
+
+import bench
+from paper_2110_04478_b200 import themis as th
+
+
+def test_hbm_bytes_closed_form_2x2x2():
+    """Per rank, RS holding H on a P_k = 2 dim reads H, writes H/2; AG holding
+    h reads and writes h: 2x2x2 totals 4.375 S for every order."""
+    S = 1 << 30
+    for pol in (th.BASELINE, th.THEMIS):
+        p = th.Plan(th.Topology((2, 2, 2), (1, 1, 1)), th.ALLREDUCE, S, 64, pol)
+        assert bench.hbm_bytes_per_rank(p, S) == 4.375 * S
+        p.close()
+
+
+def test_nvlink_bytes_equal_bus_bytes_at_one_rank_per_gpu():
+    """With every dim crossing GPUs the pulled bytes are sum_K N_K = 2S(P-1)/P (F2)."""
+    S = 1 << 30
+    p = th.Plan(th.Topology((2, 2, 2), (4, 2, 1)), th.ALLREDUCE, S, 64)
+    lay = bench.logical_layout((2, 2, 2), 8)
+    assert lay["V"] == 1 and lay["cross_gpu_dims"] == [0, 1, 2]
+    assert bench.nvlink_bytes_per_rank(p, lay["cross_gpu_dims"]) == 2 * S * 7 / 8
+    p.close()
+
+
+def test_paced_bw_exact_ratio():
+    for rat in [(4, 2, 1), (1, 1, 1), (2, 2, 1), (200, 50), (1,)]:
+        bw = bench.paced_bw(rat, 500.0)
+        assert all(Fraction(b, bw[0]) == Fraction(r, rat[0]) for b, r in zip(bw, rat))
+        assert sum(bw) <= 500_000 + 1000 * len(rat) and all(b % 1000 == 0 for b in bw)
