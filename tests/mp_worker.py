@@ -61,6 +61,52 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, ki
     return bad
 
 
+def fullsize_case(group, W, g):
+    """configs[1] at full size (2x2x2, 1 GiB fp32 per rank, 64 chunks, 4:2:1)
+    in bench.py's launch configuration for this W; sampled elements bit-exact
+    against the oracle's per-element formulation with its own schedule."""
+    import bench
+    sizes, ratio, C = (2, 2, 2), (4, 2, 1), 64
+    S_ = 1 << 30
+    N = S_ // 4
+    topo = th.Topology(sizes, ratio)
+    lay = bench.logical_layout(sizes, W)
+    V = lay["V"]
+    ncross = len(lay["cross_gpu_dims"])
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    total = sms if ncross == 0 else (32 * 3 + 32 if ncross == 3 else (sms if V >= 4 else 96))
+    comm = th.Comm(topo, S_, group=group)
+    comm.set_timeout(30.0)
+    comm.set_stages(3 if ncross == 3 else 4)
+    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, th.default_ctas(ratio, total))
+    from synth import device_input
+    xs = [device_input(g * V + v, N, "f32", torch.device("cuda")) for v in range(V)]
+    for v in range(V):
+        comm.rank_view(v, N, "f32").copy_(xs[v])
+    torch.cuda.synchronize()
+    th.run(th.ALLREDUCE, comm, plan, N, "f32")
+    torch.cuda.synchronize()
+    comm.status()
+    rng = np.random.default_rng(11)
+    idx = np.unique(np.concatenate([rng.integers(0, N, 400), [0, N - 1]]))
+    it = torch.from_numpy(idx).cuda()
+    # every rank's inputs at the sampled positions (regenerated: the generator is seeded per rank)
+    P = topo.P
+    allx = np.stack([device_input(r, N, "f32", torch.device("cuda"))[it].cpu().numpy() for r in range(P)])
+    o = T.Topology.make(sizes, ratio)
+    sched = S.schedule_collective(o, S.AR, S_, C, S.THEMIS)
+    bad = 0
+    for v in range(V):
+        got = comm.rank_view(v, N, "f32")[it].cpu().numpy()
+        for n, i in enumerate(idx):
+            b, c = O.element_location(o, N, C, int(i))
+            want = O.allreduce_element(list(allx[:, n]), o, sched.chunks[c].rs, "f32", b)
+            bad += np.float32(want).tobytes() != got[n].tobytes()
+    plan.close()
+    comm.close()
+    return bad
+
+
 def fault_case(group, W, g):
     """Fault injection: rank 1 launches a plan
     with a different intra-dimension policy.  Every rank must report
@@ -110,6 +156,10 @@ def main():
     st = fault_case(group, W, rank)
     if st != 6:
         fails.append((("fault-injection plan mismatch",), [f"status {st}"]))
+    if 8 % W == 0:
+        nb = fullsize_case(group, W, rank)
+        if nb:
+            fails.append((("full-size configs[1] sampled parity",), [f"{nb} mismatching samples"]))
     t = torch.tensor([len(fails)], device="cuda")
     dist.all_reduce(t)
     if rank == 0:
