@@ -625,6 +625,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           if (lane == 0) {
             if (u == 0) {
               if (p.trace && li == 0) p.trace[2 * opi] = dev::globaltimer();
+              if (p.tdetail && li == 0) {  // stamp 5: after a proxy fence (its cost)
+                dev::fence_proxy_async_global();
+                p.tdetail[6 * opi + 5] = dev::globaltimer();
+              }
               if (p.pace_ns_per_byte[d.dim] > 0.f) {  // group-shared pacing origin (first starter wins)
                 const unsigned long long now = dev::globaltimer();
                 const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);

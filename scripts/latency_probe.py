@@ -47,7 +47,8 @@ de = comm.fetch_trace_detail(plan).astype(np.int64)
 if rank == 0:
     st = tr[:, :, 0]
     rel = lambda x: (x - st) / 1e3
-    names = ["producer_last_tile", "consumers_done", "cta_at_counter", "last_atomic_ret", "after_sys_fence"]
+    names = ["producer_last_tile", "consumers_done", "cta_at_counter", "last_atomic_ret", "after_sys_fence",
+             "after_proxy_fence"]
     print(f"kernel {e0.elapsed_time(e1)*1e3:.1f} us  ops {st.size}")
     for j, n in enumerate(names):
         print(f"  {n:20s} median {np.median(rel(de[:, :, j])):7.2f} us  p90 {np.percentile(rel(de[:, :, j]), 90):7.2f}")
