@@ -107,6 +107,52 @@ def fullsize_case(group, W, g):
     return bad
 
 
+def nccl_and_stress_case(group, W, g, iters=60):
+    """int32 results equal torch.distributed.all_reduce (NCCL) of the per-GPU
+    sums (the library routine, SURVEY §4 tier 4), and a stress loop: many
+    back-to-back collectives with plans switching between policies / chunk
+    counts / engines on one comm, every result checked (flag protocol under
+    load: any ordering bug shows up as corruption or a watchdog timeout)."""
+    import random
+    import torch.distributed as dist
+    sizes = (2, 2, 2)
+    topo = th.Topology(sizes, (1, 1, 1))
+    P, V = 8, 8 // W
+    N = P * 256 * 4 * 4                     # divisible for C in {1, 4, 16, 64, 256}
+    comm = th.Comm(topo, N * 4, group=group)
+    comm.set_timeout(20.0)
+    rng = random.Random(1234)              # same sequence on every rank
+    plans = {}
+    bad = 0
+    for it in range(iters):
+        C = rng.choice([1, 4, 16, 64, 256])
+        pol = rng.choice([th.BASELINE, th.THEMIS])
+        intra = rng.choice([th.SCF, th.FIFO])
+        eng = rng.choice(["tma", "tma", "ldg"])
+        ctas = rng.choice([None, [4, 4, 4], [12, 6, 3]])
+        key = (C, pol, intra, str(ctas))
+        if key not in plans:
+            plans[key] = th.Plan(topo, th.ALLREDUCE, N * 4, C, pol, intra).bind(comm, ctas)
+        comm.set_engine(eng)
+        xs = [torch.randint(-(1 << 20), 1 << 20, (N,), dtype=torch.int32, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(1000 * it + g * V + v))
+              for v in range(V)]
+        for v in range(V):
+            comm.rank_view(v, N, "i32").copy_(xs[v])
+        torch.cuda.synchronize()
+        th.run(th.ALLREDUCE, comm, plans[key], N, "i32")
+        ref = torch.stack(xs).sum(0, dtype=torch.int32) if V > 1 else xs[0].clone()
+        dist.all_reduce(ref, group=group)       # NCCL over the W GPUs
+        torch.cuda.synchronize()
+        comm.status()
+        for v in range(V):
+            bad += int(not torch.equal(comm.rank_view(v, N, "i32"), ref))
+    for p_ in plans.values():
+        p_.close()
+    comm.close()
+    return bad
+
+
 def fault_case(group, W, g):
     """Fault injection: rank 1 launches a plan
     with a different intra-dimension policy.  Every rank must report
@@ -157,6 +203,9 @@ def main():
     if st != 6:
         fails.append((("fault-injection plan mismatch",), [f"status {st}"]))
     if 8 % W == 0:
+        nb = nccl_and_stress_case(group, W, rank)
+        if nb:
+            fails.append((("NCCL comparison / stress loop",), [f"{nb} mismatching results"]))
         nb = fullsize_case(group, W, rank)
         if nb:
             fails.append((("full-size configs[1] sampled parity",), [f"{nb} mismatching samples"]))
