@@ -90,6 +90,10 @@ typedef struct {
                               the min-load dim (paper uses 16) */
   int32_t charge_latency;  /* 0 (default, F5): the pre-simulation charges A_K only via
                               the tracker seed; 1: also per op */
+  int32_t concurrency;     /* ops in flight per dimension, 0/1 = one (the paper's model);
+                              k > 1: the pre-simulation runs k parallel servers of BW_K/k per
+                              dim and assigns each op a server; bound plans
+                              run server s's ops on the s-th slice of the dim's CTAs */
 } themis_plan_req_t;
 
 /* Summary of a plan.  Times in units of 1/time_scale ns, volumes in units of
@@ -142,6 +146,8 @@ themis_status_t themis_plan_orders(const themis_plan_t* plan, uint8_t* rs_order 
  * executes exactly this order on each dimension. */
 themis_status_t themis_plan_dim_ops(const themis_plan_t* plan, uint32_t* dim_ops /*[host,out] D*C*n_stages*/,
                                     int32_t* n_dim_ops /*[host,out] D*/);
+/* Server (0..concurrency-1) of every op, [C][n_stages] (all 0 for concurrency <= 1). */
+themis_status_t themis_plan_servers(const themis_plan_t* plan, int32_t* server /*[host,out] C*n_stages*/);
 /* Pre-simulated start / end time of every op, [C][n_stages], time units. */
 themis_status_t themis_plan_times(const themis_plan_t* plan, uint64_t* start /*[host,out]*/,
                                   uint64_t* end /*[host,out]*/);

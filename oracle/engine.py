@@ -61,8 +61,9 @@ class RunMetrics:
     global_order: list = field(default_factory=list)  # [(chunk, stage)] by (start, dim)
 
 
-def chunk_ops(sched: Schedule, charge_latency: bool = False) -> list:
-    """Per chunk, its ops in stage order (size before each stage)."""
+def chunk_ops(sched: Schedule, charge_latency: bool = False, servers: int = 1) -> list:
+    """Per chunk, its ops in stage order (size before each stage).
+    With `servers` parallel servers per dim each has BW_K / servers."""
     topo = sched.topo
     out = []
     for cs in sched.chunks:
@@ -71,7 +72,7 @@ def chunk_ops(sched: Schedule, charge_latency: bool = False) -> list:
         for s, (d, ph) in enumerate(cs.stages()):
             dim = topo.dims[d]
             v = bytes_sent(ph, dim.size, b)
-            dur = v / dim.bw + (fixed_delay(dim, ph) if charge_latency else 0)
+            dur = v / dim.bw * servers + (fixed_delay(dim, ph) if charge_latency else 0)
             ops.append(Op(cs.chunk, s, d, ph, b, v, dur))
             b = size_after(ph, dim.size, b)
         out.append(ops)
@@ -89,61 +90,77 @@ def _key(policy: str, op: Op, ready):
 
 
 def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
-             enforced=None) -> RunMetrics:
+             enforced=None, servers: int = 1, enforced_server=None) -> RunMetrics:
     """Run the chunk pipelines.  With `enforced` (per-dim [(chunk, stage)]),
     each dim must start its ops in exactly that order (the runtime contract,
-    PAPER.md:530); raises RuntimeError on deadlock."""
+    PAPER.md:530); raises RuntimeError on deadlock.
+
+    servers > 1 generalises R12 to PAPER.md:461/:491 ("multiple chunks per
+    dimension should be run in parallel"): each dim is `servers` parallel
+    servers with BW_K / servers each (an op takes volume*B_K*servers); idle
+    servers, in index order, each start the best ready op; m.server records
+    which server ran each op.  With enforced_server ((chunk, stage) ->
+    server), each server replays its own sub-list of `enforced` in order."""
     topo = sched.topo
     D = topo.D
-    ops = chunk_ops(sched, charge_latency)
+    ops = chunk_ops(sched, charge_latency, servers)
     total = sum(len(o) for o in ops)
     queue = [dict() for _ in range(D)]          # (chunk, stage) -> ready time
     for c, o in enumerate(ops):
         if o:
             queue[o[0].dim][(c, 0)] = Fraction(0)
-    running = [None] * D                        # (chunk, stage, end)
-    pos = [0] * D
+    running = [[None] * servers for _ in range(D)]   # (chunk, stage, end)
+    lists = None
+    if enforced is not None:
+        es = enforced_server or {}
+        lists = [[[tuple(cs) for cs in enforced[k] if es.get(tuple(cs), 0) == sv] for sv in range(servers)]
+                 for k in range(D)]
+    pos = [[0] * servers for _ in range(D)]
     m = RunMetrics(Fraction(0), [Fraction(0)] * D, [Fraction(0)] * D, [Fraction(0)] * D,
                    [Fraction(0)] * D, [[] for _ in range(D)])
+    m.server = {}
     t = Fraction(0)
     done = 0
     while done < total:
         for k in range(D):                      # starts at time t
-            if running[k] is not None or not queue[k]:
-                continue
-            if enforced is not None:
-                if pos[k] >= len(enforced[k]):
+            for sv in range(servers):
+                if running[k][sv] is not None or not queue[k]:
                     continue
-                nxt = tuple(enforced[k][pos[k]])
-                if nxt not in queue[k]:
-                    continue
-                pick = nxt
-                pos[k] += 1
-            else:
-                pick = min(queue[k], key=lambda cs: _key(policy, ops[cs[0]][cs[1]], queue[k][cs]))
-            del queue[k][pick]
-            op = ops[pick[0]][pick[1]]
-            running[k] = (pick[0], pick[1], t + op.duration)
-            m.start[pick] = t
-            m.dim_order[k].append(pick)
-            m.global_order.append(pick)
-            m.busy[k] += op.duration
-            m.volume[k] += op.volume
-        ends = [r[2] for r in running if r is not None]
+                if lists is not None:
+                    if pos[k][sv] >= len(lists[k][sv]):
+                        continue
+                    nxt = lists[k][sv][pos[k][sv]]
+                    if nxt not in queue[k]:
+                        continue
+                    pick = nxt
+                    pos[k][sv] += 1
+                else:
+                    pick = min(queue[k], key=lambda cs: _key(policy, ops[cs[0]][cs[1]], queue[k][cs]))
+                del queue[k][pick]
+                op = ops[pick[0]][pick[1]]
+                running[k][sv] = (pick[0], pick[1], t + op.duration)
+                m.start[pick] = t
+                m.server[pick] = sv
+                m.dim_order[k].append(pick)
+                m.global_order.append(pick)
+                m.busy[k] += op.duration / servers
+                m.volume[k] += op.volume
+        ends = [r[2] for rk in running for r in rk if r is not None]
         if not ends:
             raise RuntimeError("deadlock: no op running and unfinished ops remain")
         t = min(ends)
         for k in range(D):                      # completions at time t
-            r = running[k]
-            if r is None or r[2] != t:
-                continue
-            c, s, _ = r
-            running[k] = None
-            m.end[(c, s)] = t
-            m.finish[k] = t
-            done += 1
-            if s + 1 < len(ops[c]):
-                queue[ops[c][s + 1].dim][(c, s + 1)] = t
+            for sv in range(servers):
+                r = running[k][sv]
+                if r is None or r[2] != t:
+                    continue
+                c, s, _ = r
+                running[k][sv] = None
+                m.end[(c, s)] = t
+                m.finish[k] = t
+                done += 1
+                if s + 1 < len(ops[c]):
+                    queue[ops[c][s + 1].dim][(c, s + 1)] = t
     m.makespan = max(m.finish)
     m.idle = [f - b for f, b in zip(m.finish, m.busy)]
     tb = topo.total_bw

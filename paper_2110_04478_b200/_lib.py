@@ -35,7 +35,8 @@ class Topology_t(C.Structure):
 
 class PlanReq_t(C.Structure):
     _fields_ = [("coll", C.c_int32), ("policy", C.c_int32), ("intra", C.c_int32), ("n_chunks", C.c_int32),
-                ("bytes", C.c_uint64), ("threshold_div", C.c_int32), ("charge_latency", C.c_int32)]
+                ("bytes", C.c_uint64), ("threshold_div", C.c_int32), ("charge_latency", C.c_int32),
+                ("concurrency", C.c_int32)]
 
 
 class PlanInfo_t(C.Structure):
@@ -56,6 +57,7 @@ SIGNATURES = {
     "themis_plan_orders": (_ST, [_P, _P, _P]),
     "themis_plan_dim_ops": (_ST, [_P, _P, _P]),
     "themis_plan_times": (_ST, [_P, _P, _P]),
+    "themis_plan_servers": (_ST, [_P, _P]),
     "themis_plan_free": (None, [_P]),
     "themis_heap_layout": (_ST, [C.c_int32, C.c_int32, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                  C.POINTER(C.c_uint64)]),

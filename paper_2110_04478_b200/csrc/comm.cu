@@ -365,7 +365,19 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   // CTAs as it can keep busy (>= min_cta_bytes each), and consecutive ops of a
   // dimension take consecutive CTA windows, so several small chunks' ops of a
   // dimension run concurrently.  Identical on every GPU (same plan, V, caps).
-  {
+  const int SV = std::max(1, pl->req.concurrency);
+  if (SV > 1) {
+    // concurrency-aware plan: server s of dim k owns CTA slice [s*c_k/SV, (s+1)*c_k/SV)
+    // and runs exactly the ops the pre-simulation gave it, in order
+    for (int k = 0; k < D; ++k)
+      if (n[k] < SV) return fail(THEMIS_ERR_INVALID_ARG, "concurrency exceeds the CTAs of a dimension group");
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const int k = ops[i].dim, sv = pl->server[i];
+      const int o0 = sv * n[k] / SV, o1 = (sv + 1) * n[k] / SV;
+      ops[i].offset = o0;
+      ops[i].width = o1 - o0;
+    }
+  } else {
     const double slice = (double)pl->req.bytes / ((double)pl->P * pl->C);
     const double min_b = c->min_cta_bytes;
     for (int k = 0; k < D; ++k) {

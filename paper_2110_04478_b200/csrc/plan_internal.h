@@ -38,6 +38,7 @@ struct themis_plan {
   std::vector<themis::Op> ops;          // [C][NS]
   std::vector<std::vector<uint32_t>> dim_ops;  // per dim: (chunk << 8) | stage
   std::vector<themis::u128> start, end; // [C][NS]
+  std::vector<int32_t> server;          // [C][NS] pre-simulated server of each op
   std::vector<themis::u128> busy, idle, vol, load;
   themis::u128 makespan = 0, time_scale = 0, byte_scale = 0;
   uint64_t hash = 0;

@@ -75,6 +75,7 @@ themis_status_t validate(const themis_topology_t* t, const themis_plan_req_t* r)
   if (r->n_chunks < 1 || r->n_chunks > THEMIS_MAX_CHUNKS) return fail(THEMIS_ERR_INVALID_ARG, "n_chunks must be 1..1024");
   if (r->bytes == 0) return fail(THEMIS_ERR_INVALID_ARG, "bytes must be > 0");
   if (r->threshold_div < 1) return fail(THEMIS_ERR_INVALID_ARG, "threshold_div must be >= 1");
+  if (r->concurrency < 0 || r->concurrency > 64) return fail(THEMIS_ERR_INVALID_ARG, "concurrency must be 0..64");
   return THEMIS_OK;
 }
 
@@ -255,7 +256,7 @@ struct Planner {
         op.reduced_before = red;
         op.bytes_before = b;
         op.volume = is_rs ? rs_vol(b, p) : ag_vol(b, p);
-        op.duration = op.volume * W[op.dim];
+        op.duration = op.volume * W[op.dim] * (u128)std::max(1, pl.req.concurrency);  // BW_K / servers
         if (pl.req.charge_latency) op.duration += is_rs ? A_rs[op.dim] : A_ag[op.dim];
         if (is_rs) {
           b /= p;
@@ -277,11 +278,14 @@ struct Planner {
     struct Ready { int chunk, stage; u128 t; };
     std::vector<std::vector<Ready>> q(D);
     for (int c = 0; c < C; ++c) q[pl.ops[(size_t)c * NS].dim].push_back({c, 0, 0});
+    // k parallel servers per dim (concurrency <= 1: one)
+    const int SV = std::max(1, pl.req.concurrency);
     struct Run { bool on; int chunk, stage; u128 end; };
-    std::vector<Run> run(D, Run{false, 0, 0, 0});
+    std::vector<Run> run((size_t)D * SV, Run{false, 0, 0, 0});
     pl.dim_ops.assign(D, {});
     pl.start.assign(total, 0);
     pl.end.assign(total, 0);
+    pl.server.assign(total, 0);
     pl.busy.assign(D, 0);
     pl.vol.assign(D, 0);
     std::vector<u128> finish(D, 0);
@@ -304,37 +308,51 @@ struct Planner {
     u128 t = 0;
     int done = 0;
     while (done < total) {
-      for (int k = 0; k < D; ++k) {
-        if (run[k].on || q[k].empty()) continue;
-        size_t best = 0;
-        for (size_t i = 1; i < q[k].size(); ++i)
-          if (less(q[k][i], q[k][best])) best = i;
-        Ready r = q[k][best];
-        q[k].erase(q[k].begin() + best);
-        const Op& op = pl.ops[(size_t)r.chunk * NS + r.stage];
-        run[k] = Run{true, r.chunk, r.stage, t + op.duration};
-        pl.start[(size_t)r.chunk * NS + r.stage] = t;
-        pl.dim_ops[k].push_back(((uint32_t)r.chunk << 8) | (uint32_t)r.stage);
-        pl.busy[k] += op.duration;
-        pl.vol[k] += op.volume;
-      }
+      for (int k = 0; k < D; ++k)
+        for (int sv = 0; sv < SV; ++sv) {
+          Run& rk = run[(size_t)k * SV + sv];
+          if (rk.on || q[k].empty()) continue;
+          size_t best = 0;
+          for (size_t i = 1; i < q[k].size(); ++i)
+            if (less(q[k][i], q[k][best])) best = i;
+          Ready r = q[k][best];
+          q[k].erase(q[k].begin() + best);
+          const Op& op = pl.ops[(size_t)r.chunk * NS + r.stage];
+          rk = Run{true, r.chunk, r.stage, t + op.duration};
+          pl.start[(size_t)r.chunk * NS + r.stage] = t;
+          pl.server[(size_t)r.chunk * NS + r.stage] = sv;
+          pl.dim_ops[k].push_back(((uint32_t)r.chunk << 8) | (uint32_t)r.stage);
+          pl.busy[k] += op.duration;  // x SV: rescaled below
+          pl.vol[k] += op.volume;
+        }
       u128 nt = 0;
       bool any = false;
-      for (int k = 0; k < D; ++k)
-        if (run[k].on && (!any || run[k].end < nt)) {
-          nt = run[k].end;
+      for (const Run& rk : run)
+        if (rk.on && (!any || rk.end < nt)) {
+          nt = rk.end;
           any = true;
         }
       t = nt;  // always some op running: chains make progress
-      for (int k = 0; k < D; ++k) {
-        if (!run[k].on || run[k].end != t) continue;
-        run[k].on = false;
-        int c = run[k].chunk, s = run[k].stage;
-        pl.end[(size_t)c * NS + s] = t;
-        finish[k] = t;
-        ++done;
-        if (s + 1 < NS) q[pl.ops[(size_t)c * NS + s + 1].dim].push_back({c, s + 1, t});
-      }
+      for (int k = 0; k < D; ++k)
+        for (int sv = 0; sv < SV; ++sv) {
+          Run& rk = run[(size_t)k * SV + sv];
+          if (!rk.on || rk.end != t) continue;
+          rk.on = false;
+          int c = rk.chunk, s = rk.stage;
+          pl.end[(size_t)c * NS + s] = t;
+          finish[k] = t;
+          ++done;
+          if (s + 1 < NS) q[pl.ops[(size_t)c * NS + s + 1].dim].push_back({c, s + 1, t});
+        }
+    }
+    // With SV servers busy_K = sum(durations) / SV; report every time in a
+    // unit SV times finer so that all stay exact integers.
+    if (SV > 1) {
+      pl.time_scale *= SV;
+      for (auto& x : pl.start) x *= SV;
+      for (auto& x : pl.end) x *= SV;
+      for (auto& x : finish) x *= SV;
+      for (auto& x : pl.load) x *= SV;
     }
     pl.makespan = 0;
     pl.idle.assign(D, 0);
@@ -471,6 +489,12 @@ extern "C" themis_status_t themis_plan_dim_ops(const themis_plan_t* pl, uint32_t
     n_dim_ops[k] = (int32_t)pl->dim_ops[k].size();
     std::memcpy(dim_ops + k * stride, pl->dim_ops[k].data(), pl->dim_ops[k].size() * sizeof(uint32_t));
   }
+  return THEMIS_OK;
+}
+
+extern "C" themis_status_t themis_plan_servers(const themis_plan_t* pl, int32_t* server) {
+  if (!pl || !server) return fail(THEMIS_ERR_INVALID_ARG, "null argument");
+  std::memcpy(server, pl->server.data(), pl->server.size() * sizeof(int32_t));
   return THEMIS_OK;
 }
 

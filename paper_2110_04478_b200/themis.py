@@ -58,8 +58,8 @@ class Topology:
 
 
 def themis_plan(topo: Topology, coll: int, nbytes: int, n_chunks: int, policy: int = THEMIS, intra: int = SCF,
-                threshold_div: int = 16, charge_latency: bool = False) -> C.c_void_p:
-    req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency))
+                threshold_div: int = 16, charge_latency: bool = False, concurrency: int = 1) -> C.c_void_p:
+    req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency), concurrency)
     out = C.c_void_p()
     tc = topo.to_c()
     check(lib().themis_plan(C.byref(tc), C.byref(req), C.byref(out)))
@@ -71,7 +71,7 @@ class Plan:
 
     def __init__(self, topo: Topology, coll: int = ALLREDUCE, nbytes: int = 0, n_chunks: int = 64,
                  policy: int = THEMIS, intra: int = SCF, threshold_div: int = 16, charge_latency: bool = False,
-                 rs_orders=None, ag_orders=None):
+                 rs_orders=None, ag_orders=None, concurrency: int = 1):
         """rs_orders / ag_orders (C x D, 0-based): caller-given per-chunk
         orders (themis_plan_custom) instead of Algorithm 1."""
         self.topo = topo
@@ -81,9 +81,11 @@ class Plan:
         self.policy = policy
         self.intra = intra
         if rs_orders is None and ag_orders is None:
-            self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency)
+            self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency,
+                                 concurrency)
         else:
-            req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency))
+            req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency),
+                            concurrency)
             rs = None if rs_orders is None else np.ascontiguousarray(np.asarray(rs_orders, np.uint8).reshape(-1))
             ag = None if ag_orders is None else np.ascontiguousarray(np.asarray(ag_orders, np.uint8).reshape(-1))
             out = C.c_void_p()
@@ -124,6 +126,13 @@ class Plan:
             row = buf[k * C_ * NS: k * C_ * NS + n[k]]
             out.append([(int(e) >> 8, int(e) & 0xFF) for e in row])
         return out
+
+    def servers(self) -> np.ndarray:
+        """Pre-simulated server of every op, [C][n_stages]."""
+        n = self.info["n_chunks"] * self.info["n_stages"]
+        out = np.zeros(n, np.int32)
+        check(lib().themis_plan_servers(self.h, out.ctypes.data))
+        return out.reshape(self.info["n_chunks"], self.info["n_stages"])
 
     def times(self):
         n = self.info["n_chunks"] * self.info["n_stages"]

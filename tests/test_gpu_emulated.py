@@ -41,7 +41,7 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
-             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0):
+             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
@@ -50,7 +50,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_engine(engine)
     comm.set_timeout(10.0)
     comm.set_min_cta_bytes(min_cta_bytes)
-    plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra).bind(comm, ctas)
+    plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra, concurrency=concurrency).bind(comm, ctas)
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
         for it in range(repeat):
@@ -145,6 +145,16 @@ def test_op_windows_several_ops_in_flight(sizes, kinds):
     for mcb in (4096, 65536):
         check_ar(sizes, bw, "i32", 64, 516, kinds=kinds, min_cta_bytes=mcb, ctas=[12] * len(sizes))
         check_ar(sizes, bw, "f32", 16, 2052, kinds=kinds, min_cta_bytes=mcb, dist="wide")
+
+
+@pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), (Dk, Dk, Dk)), ((4, 2), (R, Dk)), ((3, 2, 2), (R, Dk, R))])
+def test_concurrency_aware_plans(sizes, kinds):
+    """Plans pre-simulated with k servers per dim run each server's ops on its
+    CTA slice (several chunks per dimension in flight)."""
+    bw = (1,) * len(sizes)
+    for k in (2, 4):
+        check_ar(sizes, bw, "i32", 64, 516, kinds=kinds, concurrency=k, ctas=[8] * len(sizes))
+        check_ar(sizes, bw, "f32", 16, 2052, kinds=kinds, concurrency=k, dist="wide")
 
 
 def test_ring_reduce_scatter_all_gather():

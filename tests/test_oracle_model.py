@@ -271,6 +271,34 @@ def test_engine_invariants_random():
                 assert E.simulate(s, E.FIFO).makespan == E.simulate(s, E.SCF).makespan
 
 
+def test_parallel_servers_per_dim():
+    """PAPER.md:461/:491 provision (several chunks per dimension in parallel):
+    `servers` parallel servers with BW_K/servers each.  Work conservation gives
+    the closed form 2*C*v/BW for a D = 1 All-Reduce whose C is a multiple of
+    the server count; busy/volume are server-count invariant; replaying the
+    recorded per-server orders reproduces the run."""
+    t = T.Topology.make((4,), (3,))
+    Sz, C = 1 << 20, 8
+    s = S.schedule_collective(t, S.AR, Sz, C, S.THEMIS)
+    v = col.bytes_sent(col.RS, 4, F(Sz, C))
+    for sv in (1, 2, 4, 8):
+        m = E.simulate(s, E.SCF, servers=sv)
+        assert m.makespan == 2 * C * v / 3
+        assert set(m.server.values()) == set(range(sv))
+    rng = random.Random(21)
+    for _ in range(20):
+        D = rng.randint(1, 3)
+        t = T.Topology.make([rng.choice([2, 3, 4]) for _ in range(D)], [rng.randint(1, 5) for _ in range(D)])
+        s = S.schedule_collective(t, S.AR, rng.randint(1, 10 ** 8), rng.randint(1, 16), S.THEMIS)
+        base = E.simulate(s, E.SCF)
+        for sv in (2, 3):
+            m = E.simulate(s, E.SCF, servers=sv)
+            assert m.busy == base.busy and m.volume == base.volume
+            assert all(m.makespan >= n / d.bw for n, d in zip(m.volume, t.dims))
+            r = E.simulate(s, E.SCF, servers=sv, enforced=m.dim_order, enforced_server=m.server)
+            assert r.start == m.start and r.makespan == m.makespan
+
+
 def test_inconsistent_order_deadlocks():
     """NPUs/dims running chunk ops in inconsistent orders
     can deadlock.  Enforcing orders where dim1 wants c1's AG before c0's RS

@@ -162,6 +162,46 @@ def test_custom_orders_full_space():
                 ag_orders=[(1, 0), (1, 0)])
 
 
+def test_concurrency_servers_bit_exact():
+    """Pre-simulation with k parallel servers per dim:
+    per-dim op order, server of every op, times, busy / idle bit-exact."""
+    rng = random.Random(515)
+    for _ in range(80):
+        D = rng.randint(1, 3)
+        sizes = [rng.choice([2, 3, 4, 8]) for _ in range(D)]
+        bw = [rng.choice(BWS) for _ in range(D)]
+        lat = [rng.choice([0, rng.randint(0, 2000)]) for _ in range(D)]
+        o, g = make_pair(sizes, bw, None, lat)
+        sv = rng.choice([2, 3, 4, 8])
+        coll = rng.choice([S.AR, S.AR, "RS", "AG"])
+        C = rng.randint(1, 40)
+        nbytes = rng.randint(1, 1 << 22) * 4096
+        pol = rng.choice([S.BASELINE, S.THEMIS])
+        intra = rng.choice([E.SCF, E.FIFO, E.SCF_LITERAL])
+        charge = rng.random() < 0.3
+        sched = S.schedule_collective(o, coll, nbytes, C, pol)
+        m = E.simulate(sched, intra, charge_latency=charge, servers=sv)
+        plan = th.Plan(g, COLLS[coll], nbytes, C, th.THEMIS if pol == S.THEMIS else th.BASELINE, INTRA[intra], 16,
+                       charge, concurrency=sv)
+        try:
+            info = plan.info
+            ts = info["time_scale"]
+            assert plan.dim_ops() == [list(x) for x in m.dim_order]
+            srv = plan.servers()
+            NS = info["n_stages"]
+            st, en = plan.times()
+            for (c, s), t0 in m.start.items():
+                assert int(srv[c, s]) == m.server[(c, s)]
+                assert Fraction(int(st[c * NS + s]), ts) == t0
+                assert Fraction(int(en[c * NS + s]), ts) == m.end[(c, s)]
+            assert Fraction(info["makespan"], ts) == m.makespan
+            assert [Fraction(b, ts) for b in info["busy"]] == m.busy
+            assert [Fraction(b, ts) for b in info["idle"]] == m.idle
+            assert [Fraction(v, ts) for v in info["final_load"]] == sched.loads
+        finally:
+            plan.close()
+
+
 def test_plan_validation_errors():
     with pytest.raises(th.ThemisError) as e:
         th.Plan(th.Topology((1, 4), (1, 1)), th.ALLREDUCE, 1024, 4)
