@@ -35,6 +35,8 @@ from paper_2110_04478_b200.dist import barrier, init_from_env, max_over_ranks  #
 from synth import WORKLOAD_PARAMS, bucket_sizes, device_input, torch_dtype  # noqa: E402
 import bench  # noqa: E402
 
+CONC = 1
+
 
 class Runner:
     def __init__(self, group, rank, world, local):
@@ -108,7 +110,8 @@ def config3(r: Runner, quick):
                         bw = bench.paced_bw(rat, pace_total) if mode == "paced" else rat
                         for pol, name in ((th.BASELINE, "baseline"), (th.THEMIS, "themis")):
                             t = th.Topology(tuple(sizes), tuple(bw))
-                            plan = th.Plan(t, th.ALLREDUCE, S, C, pol, th.SCF if pol else th.FIFO)
+                            plan = th.Plan(t, th.ALLREDUCE, S, C, pol, th.SCF if pol else th.FIFO,
+                                           concurrency=CONC)
                             plan.bind(comm, th.default_ctas(rat, r.ctas_total))
                             sec = r.time(comm, plan, th.ALLREDUCE, S // 4, "f32")
                             row[f"{mode}_{name}_bus_gbs"] = round(2 * S * (P - 1) / P / sec / 1e9, 2)
@@ -141,7 +144,7 @@ def config4(r: Runner, quick):
                     for n in buckets:
                         cnt = pad_count(n, P, C, 2)
                         plan = th.Plan(th.Topology(sizes, bw), th.ALLREDUCE, cnt * 2, C, pol,
-                                       th.SCF if pol else th.FIFO)
+                                       th.SCF if pol else th.FIFO, concurrency=CONC)
                         plan.bind(comm, th.default_ctas(rat, r.ctas_total))
                         sec = r.time(comm, plan, th.ALLREDUCE, cnt, "bf16", steps=2, warmup=1)
                         plan.close()
@@ -189,10 +192,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, required=True, choices=[3, 4, 5])
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--concurrency", type=int, default=1, help="ops in flight per dim (plans)")
     a = ap.parse_args()
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     torch.cuda.set_device(local)
+    global CONC
+    CONC = a.concurrency
     r = Runner(group, rank, world, local)
     {3: config3, 4: config4, 5: config5}[a.config](r, a.quick)
     if world > 1:
