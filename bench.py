@@ -186,7 +186,8 @@ def run_themis(a):
         # emulation); otherwise the ratio itself (only ratios matter to the plan).
         bw = paced_bw(rat, total_gbs) if total_gbs else rat
         t = th.Topology(SIZES, bw)
-        p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO)
+        p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO,
+                    concurrency=a.concurrency)
         p.bind(comm, th.default_ctas(rat, total_ctas))
         return p
 
@@ -378,6 +379,7 @@ def run_themis(a):
                         f"rank, {a.chunks} chunks, emulated BW {a.ratio}"),
                        "topology": "x".join(map(str, SIZES)), "bytes_per_rank": S, "chunks": a.chunks,
                        "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
+                       "ops_in_flight_per_dim": max(1, a.concurrency),
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
                        "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
@@ -482,6 +484,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
     ap.add_argument("--stage-kb", type=int, default=32, help="TMA ring stage size (KiB)")
+    ap.add_argument("--concurrency", type=int, default=1,
+                    help="ops in flight per dimension in the plan's pre-simulation (1 = the paper's model)")
     ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")
     ap.add_argument("--compare-ratios", default="", help="extra emulated ratios, e.g. '1:1:1,2:2:1'")
     a = ap.parse_args()
