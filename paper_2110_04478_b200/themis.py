@@ -281,7 +281,58 @@ class Comm:
         check(lib().themis_trace_fetch(self.h, out.ctypes.data, n))
         return out.reshape(plan.info["n_chunks"], plan.info["n_stages"], 2)
 
+    # -- convenience: tensors in, tensors out (copies through the heap) -------
+    def all_reduce(self, tensors, n_chunks: int = 64, policy: int = THEMIS, bw_mbps=None,
+                   ctas_per_dim: Optional[Sequence[int]] = None, stream=None):
+        """All-Reduce user tensors in place: one tensor (V = 1) or a list of V
+        tensors, one per local logical rank, same numel / dtype.
+
+        Any numel (R17): the copy into the heap is zero-padded up to the
+        executor's granule P·C·(16 B / elem), the collective runs on the
+        padded buffer (zeros add nothing) and the first numel elements are
+        copied back.  Plans are cached per (bytes, chunks, policy, bw, CTAs)
+        (PAPER.md:532).  The copies are extra HBM traffic: latency-critical
+        callers write into `rank_view` and call `themis_allreduce` directly.
+        """
+        import torch
+        ts = [tensors] if isinstance(tensors, torch.Tensor) else list(tensors)
+        if len(ts) != self.V:
+            raise ValueError(f"expected {self.V} tensors (one per local logical rank), got {len(ts)}")
+        dt = {torch.float32: "f32", torch.bfloat16: "bf16", torch.float16: "f16", torch.int32: "i32"}.get(ts[0].dtype)
+        if dt is None:
+            raise ThemisError(3, f"unsupported dtype {ts[0].dtype}")
+        n = ts[0].numel()
+        if any(t.numel() != n or t.dtype != ts[0].dtype or t.device != self.device for t in ts):
+            raise ValueError("tensors must share numel, dtype and this comm's device")
+        g = self.P * n_chunks * (16 // ELEM_SIZE[dt])
+        count = max(g, (n + g - 1) // g * g)
+        nbytes = count * ELEM_SIZE[dt]
+        if nbytes > self.vrank_stride:
+            raise ValueError(f"{nbytes} B padded exceeds the heap's {self.vrank_stride} B per rank")
+        bw = tuple(bw_mbps or self.topo.bw_mbps)
+        key = (nbytes, n_chunks, policy, bw, None if ctas_per_dim is None else tuple(ctas_per_dim))
+        cache = self.__dict__.setdefault("_plans", {})
+        plan = cache.get(key)
+        if plan is None:
+            topo = Topology(self.topo.sizes, bw, self.topo.kinds, self.topo.latency_ns)
+            plan = Plan(topo, ALLREDUCE, nbytes, n_chunks, policy, SCF if policy == THEMIS else FIFO)
+            plan.bind(self, ctas_per_dim)
+            cache[key] = plan
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        with torch.cuda.stream(s):
+            for v, t in enumerate(ts):
+                view = self.rank_view(v, count, dt)
+                view[:n].copy_(t.reshape(-1))
+                if count > n:
+                    view[n:].zero_()
+            themis_allreduce(self.data_ptr, count, dt, plan, s)
+            for v, t in enumerate(ts):
+                t.copy_(self.rank_view(v, n, dt).view(t.shape))
+        return tensors
+
     def close(self):
+        for p in self.__dict__.pop("_plans", {}).values():
+            p.close()
         if getattr(self, "h", None):
             lib().themis_comm_free(self.h)
             self.h = None

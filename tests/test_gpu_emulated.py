@@ -363,3 +363,37 @@ def test_host_buffer_entry_point():
     finally:
         plan.close()
         comm.close()
+
+
+@pytest.mark.parametrize("n,dtype", [(1, "i32"), (12345, "i32"), (1 << 16, "f32"), (77777, "bf16")])
+def test_tensor_all_reduce_any_numel(n, dtype):
+    """Comm.all_reduce: user tensors of any numel (zero-padded to the granule,
+    R17) reduce to the plain definition; int32 bit-exact, floats within the
+    north_star tolerance of the fp64 sum."""
+    topo = th.Topology((2, 2, 2), (1, 1, 1))
+    comm = th.Comm(topo, 1 << 22)
+    try:
+        xs = host_inputs(8, n, dtype)
+        ts = []
+        for r in range(8):
+            src = torch.from_numpy(xs[r].view(np.int16) if dtype == "bf16" else xs[r])
+            ts.append((src.view(torch.bfloat16) if dtype == "bf16" else src).cuda())
+        comm.all_reduce(ts, n_chunks=4)
+        if dtype == "i32":
+            comm.all_reduce(ts, n_chunks=4)             # second call reuses the cached plan
+        torch.cuda.synchronize()
+        comm.status()
+        if dtype == "i32":
+            once = O.allreduce_definition(xs, "i32")
+            want = O.allreduce_definition([once] * 8, "i32")
+            for r in range(8):
+                assert np.array_equal(ts[r].cpu().numpy(), want)
+            return
+        ref = O.allreduce_definition(xs, dtype)
+        scale = O.abs_sum(xs, dtype)
+        for r in range(8):
+            t = ts[r].cpu()
+            out = t.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else t.numpy()
+            assert np.all(np.abs(O.to_f64(out, dtype) - ref) <= TOL[dtype] * scale)
+    finally:
+        comm.close()
