@@ -212,7 +212,10 @@ themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t byte
 themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
 /* Trace: when enabled, each dim group records %globaltimer start/end of every
  * op it runs (PAPER.md:640/:658 activity).  Fetch after the stream is synced:
- * out[(chunk*n_stages + stage)*2 + {0,1}] in ns, n = C*n_stages*2 entries. */
+ * out[(chunk*n_stages + stage)*2 + {0,1}] in ns, n = C*n_stages*2 entries;
+ * start = the earliest CTA of the group that begins the op (its dependencies
+ * met), end = the op's completion published by its last CTA.  With tracing on
+ * each collective also enqueues a memset of the trace buffer before the kernel. */
 themis_status_t themis_comm_enable_trace(themis_comm_t* comm, int32_t enable);
 themis_status_t themis_trace_fetch(themis_comm_t* comm, uint64_t* out /*[host,out]*/, size_t n);
 /* Trace level 2 (themis_comm_enable_trace(comm, 2)): 6 extra %globaltimer

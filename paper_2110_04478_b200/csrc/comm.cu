@@ -503,6 +503,10 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
       if (pl->topo.kind[k] == THEMIS_DIM_RING && pl->topo.size[k] >= 3)
         return fail(THEMIS_ERR_INVALID_ARG, "ring dimensions need the TMA engine (themis_comm_set_engine(comm, 1))");
   const void* fn = kernel_for(dtype, c->engine);
+  if (c->trace_on) {  // op start = earliest working CTA (atomicMin over an all-ones start)
+    cudaError_t m = cudaMemsetAsync(c->trace, 0xFF, 2 * kMaxOps * sizeof(uint64_t), static_cast<cudaStream_t>(stream));
+    if (m != cudaSuccess) return cuda_fail(m, "cudaMemsetAsync(trace)");
+  }
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(pl->bind->total_ctas), dim3(kThreads), args,
                                               c->engine ? kSmemBytes : 0,
                                               static_cast<cudaStream_t>(stream));

@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           }
           if (lane == 0) {
             if (u == 0) {
-              if (p.trace && li == 0) p.trace[2 * opi] = dev::globaltimer();
+              if (p.trace) atomicMin(reinterpret_cast<unsigned long long*>(&p.trace[2 * opi]), dev::globaltimer());
               if (p.tdetail && li == 0) {  // stamp 5: after a proxy fence (its cost)
                 dev::fence_proxy_async_global();
                 p.tdetail[6 * opi + 5] = dev::globaltimer();
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         ok = __syncthreads_and(ok);
         if (!ok) break;
       }
-      if (p.trace && li == 0 && tid == 0) p.trace[2 * opi] = dev::globaltimer();
+      if (p.trace && tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(&p.trace[2 * opi]), dev::globaltimer());
       run_op_ldg<Tag>(p, d, li, wn);
       __syncthreads();
       if (warp == 0) complete_op_warp(p, d, opi, wn);
