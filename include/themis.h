@@ -39,6 +39,7 @@ extern "C" {
 
 #define THEMIS_MAX_DIMS 8      /* D <= 8 (the paper uses D <= 4, Table 2) */
 #define THEMIS_MAX_CHUNKS 1024 /* CPC <= 1024 (paper: 4..512) */
+#define THEMIS_AUTO_MAX_CHUNKS 256 /* largest candidate of n_chunks = 0 (auto) */
 #define THEMIS_MAX_GPUS 8      /* GPUs of one NVSwitch box */
 #define THEMIS_IPC_HANDLE_BYTES 64
 
@@ -84,7 +85,13 @@ typedef struct {
   int32_t coll;            /* themis_coll_t (CT) */
   int32_t policy;          /* themis_policy_t */
   int32_t intra;           /* themis_intra_t */
-  int32_t n_chunks;        /* CPC, 1..THEMIS_MAX_CHUNKS (paper default 64) */
+  int32_t n_chunks;        /* CPC, 1..THEMIS_MAX_CHUNKS (paper default 64);
+                              0 (themis_plan only) = auto: the power of two C <=
+                              THEMIS_AUTO_MAX_CHUNKS with bytes % (P*C*16) == 0 whose
+                              pre-simulated makespan is smallest (ties: smaller C);
+                              ALIGNMENT if bytes % (P*16) != 0.  Meaningful with
+                              step_latency_ns + charge_latency (measured A_K); the
+                              choice is themis_plan_info().n_chunks. */
   uint64_t bytes;          /* CS: bytes of the full buffer on each rank (> 0) */
   int32_t threshold_div;   /* Threshold = time of an RS/AG of chunk/threshold_div on
                               the min-load dim (paper uses 16) */

@@ -192,3 +192,23 @@ def activity_rate(m: RunMetrics, sched: Schedule, window) -> list:
             row.append(cov / (b - a))
         out.append(row)
     return out
+
+
+def choose_chunks(topo, coll: str, total_bytes: int, policy: str, intra: str = SCF, charge_latency: bool = False,
+                  servers: int = 1, max_chunks: int = 256, threshold_div: int = 16):
+    """Chunk count chosen by the pre-simulation (extension of the CPC
+    parameter; R25): among C = 1, 2, 4, ..., max_chunks
+    with total_bytes % (P * C * 16) == 0, plan each (Algorithm 1 + this engine)
+    and keep the smallest makespan; ties keep the smaller C.  Returns
+    (C, schedule, metrics), or None when no candidate divides the buffer."""
+    from .scheduler import schedule_collective
+    best = None
+    C = 1
+    while C <= max_chunks:
+        if total_bytes % (topo.P * C * 16) == 0:
+            sched = schedule_collective(topo, coll, total_bytes, C, policy, threshold_div)
+            m = simulate(sched, intra, charge_latency, servers=servers)
+            if best is None or m.makespan < best[2].makespan:
+                best = (C, sched, m)
+        C *= 2
+    return best

@@ -441,8 +441,50 @@ static themis_status_t build_plan(const themis_topology_t* topo, const themis_pl
   }
 }
 
+// n_chunks = 0: pick the chunk count (extension of PAPER.md:374 CPC, NEXT-1).
+// Candidates C = 1, 2, 4, ..., THEMIS_AUTO_MAX_CHUNKS whose 16-byte pieces tile
+// the buffer (bytes % (P * C * 16) == 0); each is planned in full and the one
+// with the smallest pre-simulated makespan wins (ties: the smaller C).  The
+// makespan only charges per-op latency with charge_latency and step_latency_ns
+// set; with A_K = 0 more chunks never lose in the model.
+static themis_status_t plan_auto_chunks(const themis_topology_t* topo, const themis_plan_req_t* req,
+                                        themis_plan_t** out) {
+  themis_plan_req_t r = *req;
+  r.n_chunks = 1;
+  themis_status_t st = validate(topo, &r);
+  if (st != THEMIS_OK) return st;
+  uint64_t P = 1;
+  for (int k = 0; k < topo->ndims; ++k) P *= (uint64_t)topo->size[k];
+  themis_plan_t* best = nullptr;
+  for (int C = 1; C <= THEMIS_AUTO_MAX_CHUNKS; C *= 2) {
+    if (req->bytes % (P * (uint64_t)C * 16u)) continue;
+    r.n_chunks = C;
+    themis_plan_t* pl = nullptr;
+    st = build_plan(topo, &r, nullptr, nullptr, false, &pl);
+    if (st != THEMIS_OK) {
+      delete best;
+      return st;
+    }
+    // makespan / time_scale, compared exactly (both fit 64 bits)
+    if (!best || (u128)pl->makespan * best->time_scale < (u128)best->makespan * pl->time_scale) {
+      delete best;
+      best = pl;
+    } else {
+      delete pl;
+    }
+  }
+  if (!best) return fail(THEMIS_ERR_ALIGNMENT, "auto chunks: bytes is not a multiple of P * 16");
+  *out = best;
+  return THEMIS_OK;
+}
+
 extern "C" themis_status_t themis_plan(const themis_topology_t* topo, const themis_plan_req_t* req,
                                        themis_plan_t** out) {
+  if (req && req->n_chunks == 0) {
+    if (!out) return fail(THEMIS_ERR_INVALID_ARG, "out is null");
+    *out = nullptr;
+    return plan_auto_chunks(topo, req, out);
+  }
   return build_plan(topo, req, nullptr, nullptr, false, out);
 }
 

@@ -26,6 +26,7 @@ SCF, FIFO, SCF_LITERAL = 0, 1, 2               # §4.3
 DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "i32": 3}
 ELEM_SIZE = {"f32": 4, "bf16": 2, "f16": 2, "i32": 4}
 COLL_NAMES = {"AR": ALLREDUCE, "RS": REDUCE_SCATTER, "AG": ALL_GATHER}
+AUTO_CHUNKS, AUTO_MAX_CHUNKS = 0, 256           # n_chunks = 0: planner picks C (THEMIS_AUTO_MAX_CHUNKS)
 
 
 @dataclass(frozen=True)
@@ -103,6 +104,7 @@ class Plan:
             "makespan": i.makespan, "busy": list(i.busy[:D]), "idle": list(i.idle[:D]),
             "dim_volume": list(i.dim_volume[:D]), "final_load": list(i.final_load[:D]), "hash": i.hash,
         }
+        self.n_chunks = i.n_chunks          # the planner's choice when n_chunks = 0 (auto)
 
     # -- queries -------------------------------------------------------------
     @property
@@ -304,7 +306,7 @@ class Comm:
         n = ts[0].numel()
         if any(t.numel() != n or t.dtype != ts[0].dtype or t.device != self.device for t in ts):
             raise ValueError("tensors must share numel, dtype and this comm's device")
-        g = self.P * n_chunks * (16 // ELEM_SIZE[dt])
+        g = self.P * (n_chunks or AUTO_MAX_CHUNKS) * (16 // ELEM_SIZE[dt])   # 0 = auto: every candidate fits
         count = max(g, (n + g - 1) // g * g)
         nbytes = count * ELEM_SIZE[dt]
         if nbytes > self.vrank_stride:

@@ -13,7 +13,8 @@ executor from device traces and feeds them back into the planner:
    with the makespan the pre-simulation predicts from (A_K, BW_K) with
    `charge_latency` on, and with the paper's bandwidth-only model, and the
    latency-aware Themis plan (tracker seeded with A_K, A charged per op) is
-   timed against the plain Themis plan and the baseline.
+   timed against the plain Themis plan and the baseline; finally the planner
+   also picks the chunk count (n_chunks = 0) from the calibrated model.
 
     python scripts/calibrate.py [--ratio 4:2:1] [--paced]
     torchrun --nproc-per-node 4 --master-addr 127.0.0.1 scripts/calibrate.py --gpus 4
@@ -157,6 +158,7 @@ def main():
     # 3. validation: model vs measured; latency-aware Themis vs plain Themis vs baseline
     cal = th.Topology(sizes, bw_cal, None, lat_cal)
     for mib in (1, 4, 16, 64, 256):
+        fixed = {}
         for C in (4, 16, 64):
             nbytes = mib << 20
             cnt = nbytes // 4
@@ -189,7 +191,22 @@ def main():
             if "us" in row.get("themis", {}) and "us" in row.get("themis_latency_aware", {}):
                 row["latency_aware_vs_plain"] = round(row["themis"]["us"] / row["themis_latency_aware"]["us"], 3)
                 row["latency_aware_vs_baseline"] = round(row["baseline"]["us"] / row["themis_latency_aware"]["us"], 3)
+                fixed[C] = row
             emit(row)
+        # n_chunks = 0: the latency-aware planner also picks the chunk count
+        nbytes = mib << 20
+        pa = th.Plan(cal, th.ALLREDUCE, nbytes, th.AUTO_CHUNKS, th.THEMIS, th.SCF, charge_latency=True).bind(comm, ctas)
+        t, _ = timed(pa, nbytes // 4, a.steps)
+        row = {"mib": mib, "chunks": "auto", "chosen_chunks": pa.n_chunks, "n_gpus": world, "ratio": a.ratio,
+               "mode": "paced" if a.paced else "caps", "themis_auto": {"us": round(t / 1e3, 2),
+               "model_latency_us": round(float(pa.makespan_ns()) / 1e3, 2)}}
+        pa.close()
+        if 64 in fixed:
+            row["auto_vs_themis_c64"] = round(fixed[64]["themis"]["us"] * 1e3 / t, 3)
+            row["auto_vs_baseline_c64"] = round(fixed[64]["baseline"]["us"] * 1e3 / t, 3)
+        best = min((r["themis_latency_aware"]["us"], C) for C, r in fixed.items())
+        row["best_fixed_latency_aware"] = {"us": best[0], "chunks": best[1]}
+        emit(row)
     comm.close()
     if world > 1:
         import torch.distributed as dist

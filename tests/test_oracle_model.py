@@ -423,3 +423,36 @@ def test_export_csv():
     lines = S.export_csv(s).strip().split("\n")
     assert lines[0] == "chunk_id,rs_order,ag_order,bytes"
     assert lines[2].startswith("1,2 1,1 2,")
+
+
+def test_choose_chunks_single_dim_closed_form():
+    """D = 1: the one dim serves all 2C ops back to back, so the makespan is
+    2C*A + 2S(P-1)/P * B (PAPER.md:468 with idle = 0): strictly increasing in C
+    when A > 0 (choice C = 1), constant when A = 0 (tie -> smallest C = 1)."""
+    from fractions import Fraction as F
+    from oracle import engine as E, scheduler as S, topology as T
+    S_ = 1 << 20
+    for lat in (0, 1000):
+        t = T.Topology.make((4,), [F(100)], [T.DIRECT], [lat])
+        best = E.choose_chunks(t, S.AR, S_, S.THEMIS, E.SCF, charge_latency=True)
+        assert best[0] == 1
+        for C in (1, 2, 8, 64):
+            m = E.simulate(S.schedule_collective(t, S.AR, S_, C, S.THEMIS), E.SCF, charge_latency=True)
+            assert m.makespan == 2 * C * lat + F(2 * S_ * 3, 4) / 100
+    assert E.choose_chunks(T.Topology.make((4,), [F(100)]), S.AR, 4 * 16 + 8, S.THEMIS) is None
+
+
+def test_choose_chunks_pipelining_without_latency():
+    """D = 2, A = 0: one chunk cannot overlap the two dims (makespan = the sum
+    of its four stage times), many chunks approach the Ideal bound (R13), so
+    the choice is never C = 1 and its makespan is within the pipeline fill of
+    the Ideal."""
+    from fractions import Fraction as F
+    from oracle import engine as E, scheduler as S, topology as T
+    t = T.Topology.make((2, 2), [F(100), F(100)])
+    S_ = 1 << 22
+    C, sched, m = E.choose_chunks(t, S.AR, S_, S.BASELINE, E.FIFO)
+    one = E.simulate(S.schedule_collective(t, S.AR, S_, 1, S.BASELINE), E.FIFO)
+    assert one.makespan == (F(S_, 2) + F(S_, 4) + F(S_, 4) + F(S_, 2)) / 100   # chain of 4 stages, nothing overlaps
+    assert C > 1 and m.makespan < one.makespan
+    assert m.makespan >= E.ideal_time(sched)

@@ -211,7 +211,9 @@ def test_plan_validation_errors():
     with pytest.raises(th.ThemisError):
         th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 0, 4)
     with pytest.raises(th.ThemisError):
-        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1024, 0)
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1024, -1)
+    with pytest.raises(th.ThemisError):                       # n_chunks = 0 (auto) is custom-orders-free only
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1024, 0, rs_orders=[[0, 1]], ag_orders=[[1, 0]])
     with pytest.raises(th.ThemisError):
         th.Plan(th.Topology((2, 2), (1, 0)), th.ALLREDUCE, 1024, 4)
 
@@ -230,3 +232,33 @@ def test_plan_hash_deterministic():
     b = th.Plan(g, th.ALLREDUCE, 1 << 30, 64)
     c = th.Plan(g, th.ALLREDUCE, 1 << 30, 64, policy=th.BASELINE)
     assert a.info["hash"] == b.info["hash"] != c.info["hash"]
+
+
+@pytest.mark.parametrize("sizes,bw,lat,nbytes,pol", [
+    ((2, 2, 2), (80000, 80000, 80000), (8000, 9000, 8500), 1 << 20, S.THEMIS),    # calibrated A_K (profiles/r01/calibration)
+    ((2, 2, 2), (80000, 80000, 80000), (8000, 9000, 8500), 64 << 20, S.THEMIS),
+    ((2, 2, 2), (80000, 80000, 80000), (8000, 9000, 8500), 1 << 30, S.BASELINE),
+    ((4, 2), (200000, 50000), (500, 2000), 16 << 20, S.THEMIS),
+    ((2, 4), (100000, 100000), (0, 0), 4 << 20, S.THEMIS),                          # A = 0: ties / pipelining
+    ((8,), (300000,), (1000,), 1 << 24, S.THEMIS),
+])
+def test_auto_chunks_parity(sizes, bw, lat, nbytes, pol):
+    """n_chunks = 0: the C++ planner picks the same C as the oracle's
+    choose_chunks and the resulting plan is bit-identical."""
+    o, g = make_pair(sizes, bw, lat=list(lat))
+    want = E.choose_chunks(o, S.AR, nbytes, pol, E.SCF if pol == S.THEMIS else E.FIFO, charge_latency=True)
+    plan = th.Plan(g, th.ALLREDUCE, nbytes, th.AUTO_CHUNKS, th.THEMIS if pol == S.THEMIS else th.BASELINE,
+                   th.SCF if pol == S.THEMIS else th.FIFO, charge_latency=True)
+    try:
+        assert plan.n_chunks == want[0]
+        assert Fraction(plan.info["makespan"], plan.info["time_scale"]) == want[2].makespan
+    finally:
+        plan.close()
+    compare(o, g, S.AR, nbytes, want[0], pol, E.SCF if pol == S.THEMIS else E.FIFO, charge=True)
+
+
+def test_auto_chunks_alignment_error():
+    g = th.Topology((2, 2), (1000, 1000))
+    with pytest.raises(th.ThemisError) as e:
+        th.Plan(g, th.ALLREDUCE, 4 * 16 + 8, th.AUTO_CHUNKS)
+    assert e.value.status == 2          # THEMIS_ERR_ALIGNMENT
