@@ -78,3 +78,48 @@ def test_config2_full_size(dtype):
     finally:
         plan.close()
         comm.close()
+
+
+def test_max_size_bf16_over_2pow31_elements():
+    """Maximum-size edge case: 2^31 + 2^25 bf16 elements (4.06 GiB) per rank,
+    8 ranks in one GPU (33 GB heap): element indices exceed int32 and byte
+    offsets exceed 32 bits.  Every rank bitwise identical; sampled elements
+    (including both ends of every block) bit-exact vs the oracle's
+    per-element formulation with the oracle's Themis schedule at 1:1:1."""
+    ratio = (1, 1, 1)
+    topo = th.Topology(SIZES, ratio)
+    P = topo.P
+    N = (1 << 31) + (1 << 25)
+    S_ = N * 2
+    comm = th.Comm(topo, S_)
+    comm.set_timeout(60.0)
+    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm)
+    try:
+        rng = np.random.default_rng(11)
+        blk = N // P
+        idx = np.unique(np.concatenate([rng.integers(0, N, 800), [b * blk for b in range(P)],
+                                        [b * blk + blk - 1 for b in range(P)], [(1 << 31) - 1, 1 << 31, N - 1]]))
+        it = torch.from_numpy(idx).cuda()
+        xv = []
+        for r in range(P):
+            x = device_input(r, N, "bf16", torch.device("cuda", 0))
+            comm.rank_view(r, N, "bf16").copy_(x)
+            xv.append(x[it].view(torch.int16).cpu().numpy().view(np.uint16))
+            del x
+        th.run(th.ALLREDUCE, comm, plan, N, "bf16")
+        torch.cuda.synchronize()
+        comm.status()
+        outs = [comm.rank_view(r, N, "bf16") for r in range(P)]
+        for r in range(1, P):
+            assert torch.equal(outs[r].view(torch.int16), outs[0].view(torch.int16))
+        got = outs[0][it].view(torch.int16).cpu().numpy().view(np.uint16)
+        o = T.Topology.make(SIZES, ratio)
+        sched = S.schedule_collective(o, S.AR, S_, C, S.THEMIS)
+        xv = np.stack(xv)
+        for n, i in enumerate(idx):
+            b, c = O.element_location(o, N, C, int(i))
+            v = O.allreduce_element(list(xv[:, n]), o, sched.chunks[c].rs, "bf16", b)
+            assert np.asarray(v).view(np.uint16).ravel()[0] == got[n], f"element {i}"
+    finally:
+        plan.close()
+        comm.close()
