@@ -253,7 +253,10 @@ themis_status_t themis_plan_bound_ctas(const themis_plan_t* plan, int32_t* ctas_
  * (ALIGNMENT); the plan's coll matches the call (PLAN_MISMATCH); all ranks
  * call the same collectives, with identical plans, in the same order.
  * Float sums: fp32 accumulate in coordinate order within each stage, one
- * round-to-nearest-even per RS stage for bf16/f16 (R18); int32 wraps (R19). */
+ * round-to-nearest-even per RS stage for bf16/f16 (R18); int32 wraps (R19).
+ * Each call is one cooperative kernel launch on `stream` and may be captured
+ * into a CUDA graph: the collective epoch is kept on the device, so every
+ * replay is a new collective (all ranks must replay the same sequence). */
 themis_status_t themis_allreduce(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
 themis_status_t themis_reduce_scatter(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);
 themis_status_t themis_all_gather(void* buf, uint64_t count, int32_t dtype, const themis_plan_t* plan, void* stream);

@@ -70,11 +70,11 @@ struct themis_comm {
   themis_topology_t topo{};
   char* heap[THEMIS_MAX_GPUS] = {};
   uint64_t heap_bytes = 0, vrank_stride = 0, sig_bytes = 0;
-  uint32_t epoch = 0;
   uint32_t* opcnt = nullptr;
   unsigned long long* op_t0 = nullptr;
   uint32_t* done_cnt = nullptr;
   uint32_t* abort_flag = nullptr;
+  uint32_t* epoch_ctr = nullptr;  // device-resident collective epoch (graph-replay safe)
   uint32_t* herr_host = nullptr;
   uint32_t* herr_dev = nullptr;
   uint64_t* trace = nullptr;
@@ -188,6 +188,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   *c->herr_host = 0;
   c->done_cnt = c->opcnt + kMaxOps;
   c->abort_flag = c->opcnt + kMaxOps + 1;
+  c->epoch_ctr = c->opcnt + kMaxOps + 2;
   int nb = 0;
   if ((e = prepare_kernels()) != cudaSuccess ||
       (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, themis_exec_kernel<dev::F32Tag, true>, kThreads,
@@ -474,7 +475,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.blk_elems = count / c->P;
   kp.slice_elems = count / ((uint64_t)c->P * pl->C);
   kp.elem_size = esz;
-  kp.epoch = ++c->epoch;
+  kp.epoch_ctr = c->epoch_ctr;
   kp.opcnt = c->opcnt;
   kp.op_t0 = c->op_t0;
   kp.done_cnt = c->done_cnt;

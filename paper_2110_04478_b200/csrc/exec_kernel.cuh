@@ -49,7 +49,7 @@ struct KParams {
   uint64_t blk_elems;       // N / P
   uint64_t slice_elems;     // N / (P*C)
   int32_t elem_size;
-  uint32_t epoch;
+  uint32_t* epoch_ctr;      // device: epoch of the last completed collective on this comm
   unsigned long long plan_hash;  // must be identical on every rank (checked at entry)
   uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
   unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
@@ -103,6 +103,11 @@ __device__ __forceinline__ int ring_peer(const KParams& p, int q, int k, int del
 }
 
 // Spin until *f >= e.  Returns false on timeout / abort (watchdog).
+// This launch's epoch (a6), read once per CTA from the comm's device counter
+// (so a collective captured in a CUDA graph gets a fresh epoch on every replay).
+__shared__ uint32_t s_epoch;
+__device__ __forceinline__ uint32_t cur_epoch() { return s_epoch; }
+
 __device__ bool wait_geq(const KParams& p, const uint32_t* f, uint32_t e, uint32_t where) {
   if (dev::ld_acquire_sys(f) >= e) return true;
   const uint64_t t0 = dev::globaltimer();
@@ -455,7 +460,7 @@ __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d
   for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
     const int q = q0 + t / pk;
     const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
   }
   return __all_sync(0xFFFFFFFFu, ok);
 }
@@ -471,7 +476,7 @@ __device__ __forceinline__ bool wait_ring_warp(const KParams& p, const OpDesc& d
   bool ok = true;
   for (int v = threadIdx.x & 31; v < V; v += 32) {
     const int q = q0 + v;
-    ok &= wait_geq64(p, ring_slot(p, q, ring_peer(p, q, k, -1), k, gi), ring_flag_value(p.epoch, d.seq, step),
+    ok &= wait_geq64(p, ring_slot(p, q, ring_peer(p, q, k, -1), k, gi), ring_flag_value(cur_epoch(), d.seq, step),
                      0xFFFFFCu);
   }
   return __all_sync(0xFFFFFFFFu, ok);
@@ -492,7 +497,7 @@ __device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc
   __syncwarp();
   for (int v = lane; v < V; v += 32) {
     const int q = q0 + v;
-    dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(p.epoch, d.seq, step + 1));
+    dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(cur_epoch(), d.seq, step + 1));
   }
   __syncwarp();
 }
@@ -538,9 +543,9 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
       const int q = q0 + t / pn;
       const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
       if (local)
-        dev::st_relaxed_gpu(ready_slot(p, dst, q, opi), p.epoch);
+        dev::st_relaxed_gpu(ready_slot(p, dst, q, opi), cur_epoch());
       else
-        dev::st_relaxed_sys(ready_slot(p, dst, q, opi), p.epoch);
+        dev::st_relaxed_sys(ready_slot(p, dst, q, opi), cur_epoch());
     }
   }
   if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
@@ -562,6 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
   const int V = p.V, P = p.P;
   const int q0 = p.my_gpu * V;
   bool ok = true;
+  // epoch = 1 + that of the previous collective on this comm (stream order:
+  // the previous kernel stored it after every CTA had read its own).
+  if (tid == 0) s_epoch = *(volatile uint32_t*)p.epoch_ctr + 1u;
   if (kTma && tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       dev::mbar_init(&full[s], 1);
@@ -573,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     }
     dev::fence_mbar_init();
   }
+  __syncthreads();
 
   // a6: entry barrier — every local rank announces the epoch (and, ordered
   // before it by the release, its plan hash) to every rank.  Inter-dimension
@@ -581,10 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
   if (blockIdx.x == 0)
     for (int i = tid; i < V * P; i += blockDim.x) {
       dev::st_relaxed_sys64(hash_slot(p, i % P, q0 + i / P), p.plan_hash);
-      dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), p.epoch);
+      dev::st_release_sys(entry_slot(p, i % P, q0 + i / P), cur_epoch());
     }
   for (int i = tid; i < V * P; i += blockDim.x) {
-    ok &= wait_geq(p, entry_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFFu);
+    ok &= wait_geq(p, entry_slot(p, q0 + i / P, i % P), cur_epoch(), 0xFFFFFFu);
     if (ok && *(volatile unsigned long long*)hash_slot(p, q0 + i / P, i % P) != p.plan_hash) {
       ok = false;
       atomicExch(p.abort_flag, 1u);
@@ -716,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         for (int t = tid; t < V * pk; t += blockDim.x) {
           const int q = q0 + t / pk;
           const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), p.epoch, (uint32_t)opi);
+          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
         }
         ok = __syncthreads_and(ok);
         if (!ok) break;
@@ -742,6 +751,9 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     __threadfence_system();
   }
   __syncthreads();
-  for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(exit_slot(p, i % P, q0 + i / P), p.epoch);
-  for (int i = tid; i < V * P; i += blockDim.x) wait_geq(p, exit_slot(p, q0 + i / P, i % P), p.epoch, 0xFFFFFDu);
+  for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(exit_slot(p, i % P, q0 + i / P), cur_epoch());
+  for (int i = tid; i < V * P; i += blockDim.x) wait_geq(p, exit_slot(p, q0 + i / P, i % P), cur_epoch(), 0xFFFFFDu);
+  // every CTA has read the epoch (all counted in done_cnt): advance it for the next launch
+  __syncthreads();
+  if (tid == 0) *(volatile uint32_t*)p.epoch_ctr = cur_epoch();
 }

@@ -397,3 +397,45 @@ def test_tensor_all_reduce_any_numel(n, dtype):
             assert np.all(np.abs(O.to_f64(out, dtype) - ref) <= TOL[dtype] * scale)
     finally:
         comm.close()
+
+
+def test_cuda_graph_capture_and_replay():
+    """Collectives captured in a CUDA graph replay correctly: the epoch lives
+    on the device (a6), so each replay is a fresh collective.  int32 exact:
+    two All-Reduces per graph, three replays = six All-Reduces in a row."""
+    topo = th.Topology((2, 2, 2), (1, 1, 1))
+    P, C_ = 8, 4
+    N = P * C_ * 1024
+    comm = th.Comm(topo, N * 4)
+    comm.set_timeout(10.0)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm)
+    try:
+        xs = host_inputs(P, N, "i32")
+        for r in range(P):
+            comm.rank_view(r, N, "i32").copy_(torch.from_numpy(xs[r]))
+        th.run(th.ALLREDUCE, comm, plan, N, "i32")            # eager call first (epoch 1)
+        torch.cuda.synchronize()
+        want = O.allreduce_definition(xs, "i32")
+        assert np.array_equal(comm.rank_view(3, N, "i32").cpu().numpy(), want)
+        for r in range(P):                                     # restart from the inputs
+            comm.rank_view(r, N, "i32").copy_(torch.from_numpy(xs[r]))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                th.run(th.ALLREDUCE, comm, plan, N, "i32")
+                th.run(th.ALLREDUCE, comm, plan, N, "i32")
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        comm.status()
+        want = xs
+        for _ in range(6):
+            want = [O.allreduce_definition(want, "i32")] * P
+        for r in range(P):
+            assert np.array_equal(comm.rank_view(r, N, "i32").cpu().numpy(), want[0]), f"rank {r}"
+    finally:
+        plan.close()
+        comm.close()
