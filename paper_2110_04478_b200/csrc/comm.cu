@@ -10,6 +10,7 @@
 //       coordinate order, stored in place   (R16, R18)
 //   AG: copies every peer j's held blocks (digit_k = j) into v's buffer.
 // Capping c_k emulates per-dimension bandwidth (BASELINE.json north_star (d)).
+#include <cuda.h>  // driver types for the stream memory ops (entry points fetched at run time, no -lcuda)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -87,6 +88,11 @@ struct themis_comm {
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
+  // host-buffer streaming (themis_allreduce_host), created on first use
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  uint32_t* d2h_flags = nullptr;  // [THEMIS_MAX_CHUNKS] device
+  uint32_t host_seq = 0;
 };
 
 namespace themis {
@@ -210,6 +216,15 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
 
 extern "C" void themis_comm_free(themis_comm_t* c) {
   if (!c) return;
+  if (c->h2d) {
+    cudaStreamSynchronize(c->h2d);
+    cudaStreamSynchronize(c->d2h);
+    cudaStreamDestroy(c->h2d);
+    cudaStreamDestroy(c->d2h);
+    cudaEventDestroy(c->ev_in);
+    cudaEventDestroy(c->ev_out);
+    cudaFree(c->d2h_flags);
+  }
   cudaFree(c->opcnt);
   cudaFree(c->op_t0);
   cudaFree(c->trace);
@@ -424,8 +439,8 @@ extern "C" themis_status_t themis_plan_bound_ctas(const themis_plan_t* pl, int32
   return THEMIS_OK;
 }
 
-static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype, const themis_plan_t* pl,
-                              void* stream) {
+static themis_status_t check_call(int coll, void* buf, uint64_t count, int32_t dtype, const themis_plan_t* pl,
+                                  int* esz_out) {
   if (!pl || !pl->bind) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan is not bound to a comm");
   if (pl->req.coll != coll) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan was made for another collective");
   themis_comm* c = pl->bind->comm;
@@ -449,7 +464,18 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
       (uint64_t)(p - mine - data0) + count * esz > c->vrank_stride)
     return fail(THEMIS_ERR_NOT_REGISTERED, "buf is not inside the comm's heap data region");
   if (reinterpret_cast<uintptr_t>(p) % 16) return fail(THEMIS_ERR_ALIGNMENT, "buf must be 16-byte aligned");
+  *esz_out = esz;
+  return THEMIS_OK;
+}
 
+static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype, const themis_plan_t* pl,
+                              void* stream, uint32_t host_seq = 0) {
+  int esz = 0;
+  themis_status_t st = check_call(coll, buf, count, dtype, pl, &esz);
+  if (st != THEMIS_OK) return st;
+  themis_comm* c = pl->bind->comm;
+  char* mine = c->heap[c->gpu_rank];
+  char* p = static_cast<char*>(buf);
   KParams kp{};
   kp.D = pl->D;
   kp.P = c->P;
@@ -494,6 +520,8 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;
   kp.ag_rr = c->ag_rr;
+  kp.host_seq = host_seq;
+  kp.d2h_flags = c->d2h_flags;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
@@ -526,21 +554,95 @@ extern "C" themis_status_t themis_all_gather(void* buf, uint64_t count, int32_t 
   return launch(THEMIS_ALL_GATHER, buf, count, dtype, pl, stream);
 }
 
+// Stream memory ops (write / wait on a 32-bit device word) from the driver,
+// fetched through the runtime so the library needs no -lcuda at link time.
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WriteValue32Fn g_write32 = nullptr;
+static WaitValue32Fn g_wait32 = nullptr;
+
+static themis_status_t host_stream_setup(themis_comm* c) {
+  if (c->h2d) return THEMIS_OK;
+  if (!g_write32 || !g_wait32) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void *w = nullptr, *t = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1));
+    CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2));
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !t)
+      return fail(THEMIS_ERR_CUDA, "driver stream memory ops unavailable");
+    g_write32 = reinterpret_cast<WriteValue32Fn>(w);
+    g_wait32 = reinterpret_cast<WaitValue32Fn>(t);
+  }
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+  CUDA_TRY(cudaMalloc(&c->d2h_flags, sizeof(uint32_t) * THEMIS_MAX_CHUNKS));
+  CUDA_TRY(cudaMemset(c->d2h_flags, 0, sizeof(uint32_t) * THEMIS_MAX_CHUNKS));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return THEMIS_OK;
+}
+
+// Host buffers in and out, streamed chunk by chunk so PCIe overlaps the
+// collective: an H2D stream copies chunk c of every local rank (one 2-D copy
+// per rank: P slices of slice bytes, block pitch) and then writes the chunk's
+// h2d flag (= this call's sequence number) into local rank 0's signal pad; the
+// kernel's stage-0 op of chunk c waits for the flags of every source GPU; the
+// last stage of chunk c publishes a d2h flag that a D2H stream waits on
+// before copying the chunk back.  Chunks are fed in the order of their
+// pre-simulated stage-0 start and drained in the order of their final-stage
+// end.  The user stream waits for the D2H stream at the end, so stream order
+// semantics are those of a single call.
 extern "C" themis_status_t themis_allreduce_host(const void* host_in, void* host_out, void* buf, uint64_t count,
                                                  int32_t dtype, const themis_plan_t* pl, void* stream) {
   if (!pl || !pl->bind) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan is not bound to a comm");
   if (!host_in || !host_out) return fail(THEMIS_ERR_INVALID_ARG, "null host buffer");
-  themis_comm* c = pl->bind->comm;
-  const uint64_t bytes = pl->req.bytes;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int v = 0; v < c->V; ++v)
-    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(buf) + v * c->vrank_stride, static_cast<const char*>(host_in) + v * bytes,
-                             bytes, cudaMemcpyHostToDevice, s));
-  themis_status_t st = themis_allreduce(buf, count, dtype, pl, stream);
+  if (pl->req.coll != THEMIS_ALLREDUCE) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan was made for another collective");
+  int esz = 0;
+  themis_status_t st = check_call(THEMIS_ALLREDUCE, buf, count, dtype, pl, &esz);  // before any copy lands
   if (st != THEMIS_OK) return st;
-  for (int v = 0; v < c->V; ++v)
-    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(host_out) + v * bytes, static_cast<char*>(buf) + v * c->vrank_stride,
-                             bytes, cudaMemcpyDeviceToHost, s));
+  themis_comm* c = pl->bind->comm;
+  if ((st = host_stream_setup(c)) != THEMIS_OK) return st;
+  const uint64_t bytes = pl->req.bytes;
+  const int P = c->P, C = pl->C, NS = pl->NS;
+  const uint64_t blk = bytes / P, slice = blk / C;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t seq = ++c->host_seq;
+  // the copy streams start after the user stream's prior work (incl. the
+  // previous collective on this comm, hence every peer's reads of our buffer)
+  CUDA_TRY(cudaEventRecord(c->ev_in, s));
+  CUDA_TRY(cudaStreamWaitEvent(c->h2d, c->ev_in, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->ev_in, 0));
+  std::vector<int> in_order(C), out_order(C);
+  for (int i = 0; i < C; ++i) in_order[i] = out_order[i] = i;
+  std::stable_sort(in_order.begin(), in_order.end(),
+                   [&](int a, int b) { return pl->start[(size_t)a * NS] < pl->start[(size_t)b * NS]; });
+  std::stable_sort(out_order.begin(), out_order.end(), [&](int a, int b) {
+    return pl->end[(size_t)a * NS + NS - 1] < pl->end[(size_t)b * NS + NS - 1];
+  });
+  char* pad0 = c->heap[c->gpu_rank];  // local rank 0's signal pad
+  for (int ch : in_order) {
+    for (int v = 0; v < c->V; ++v)
+      CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(buf) + v * c->vrank_stride + ch * slice, blk,
+                                 static_cast<const char*>(host_in) + v * bytes + ch * slice, blk, slice, P,
+                                 cudaMemcpyHostToDevice, c->h2d));
+    const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(pad0 + h2d_offset(P) + 4ull * ch);
+    if (g_write32(reinterpret_cast<CUstream>(c->h2d), flag, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(THEMIS_ERR_CUDA, "cuStreamWriteValue32 (h2d flag)");
+  }
+  st = launch(THEMIS_ALLREDUCE, buf, count, dtype, pl, stream, seq);
+  if (st != THEMIS_OK) return st;
+  for (int ch : out_order) {
+    const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(c->d2h_flags + ch);
+    if (g_wait32(reinterpret_cast<CUstream>(c->d2h), flag, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(THEMIS_ERR_CUDA, "cuStreamWaitValue32 (d2h flag)");
+    for (int v = 0; v < c->V; ++v)
+      CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(host_out) + v * bytes + ch * slice, blk,
+                                 static_cast<char*>(buf) + v * c->vrank_stride + ch * slice, blk, slice, P,
+                                 cudaMemcpyDeviceToHost, c->d2h));
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_out, c->d2h));
+  CUDA_TRY(cudaStreamWaitEvent(s, c->ev_out, 0));
   return THEMIS_OK;
 }
 

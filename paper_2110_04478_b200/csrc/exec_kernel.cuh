@@ -63,6 +63,8 @@ struct KParams {
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
+  uint32_t host_seq;        // host-buffer streaming (themis_allreduce_host): value of this call's h2d / d2h flags; 0 = off
+  uint32_t* d2h_flags;      // [THEMIS_MAX_CHUNKS] device: chunk c final on this GPU (read by a stream wait op)
 };
 
 // ---------------------------------------------------------------- signal pads
@@ -71,7 +73,9 @@ __host__ __device__ __forceinline__ uint64_t ring_flags_offset(int P) { return 4
 __host__ __device__ __forceinline__ uint64_t hash_offset(int P) {
   return ring_flags_offset(P) + 8ull * P * THEMIS_MAX_DIMS * kMaxCtas;
 }
-__host__ __device__ __forceinline__ uint64_t pad_bytes(int P) { return hash_offset(P) + 8ull * P; }
+__host__ __device__ __forceinline__ uint64_t h2d_offset(int P) { return hash_offset(P) + 8ull * P; }
+// pad(q) continues: [hash u64 P][h2d u32 THEMIS_MAX_CHUNKS] (h2d used in local rank 0's pad only)
+__host__ __device__ __forceinline__ uint64_t pad_bytes(int P) { return h2d_offset(P) + 4ull * THEMIS_MAX_CHUNKS; }
 __device__ __forceinline__ uint32_t* sig_of(const KParams& p, int q) {
   return reinterpret_cast<uint32_t*>(p.heap[q / p.V] + (uint64_t)(q % p.V) * p.sig_bytes);
 }
@@ -88,6 +92,11 @@ __device__ __forceinline__ unsigned long long* ring_slot(const KParams& p, int q
 // plan hash announced by rank `src` for the current call, in q's pad
 __device__ __forceinline__ unsigned long long* hash_slot(const KParams& p, int q, int src) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sig_of(p, q)) + hash_offset(p.P)) + src;
+}
+// host-buffer streaming: chunk c of GPU g's local ranks has arrived from the
+// host (written by a stream memory op after the copies, value = host_seq)
+__device__ __forceinline__ uint32_t* h2d_slot(const KParams& p, int g, int c) {
+  return reinterpret_cast<uint32_t*>(p.heap[g] + h2d_offset(p.P)) + c;
 }
 __device__ __forceinline__ char* data_of(const KParams& p, int q) {
   return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
@@ -454,13 +463,18 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
 }
 
 // One warp: wait until the local ranks and their dim-k peers completed (c, s-1).
+// Stage s > 0: every source finished (c, s-1).  Stage 0 in host-buffer mode:
+// every source GPU's copy of chunk c has landed (h2d flag = host_seq).
 __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d, int opi) {
   const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
   bool ok = true;
   for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
     const int q = q0 + t / pk;
     const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-    ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
+    if (d.stage > 0)
+      ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
+    else
+      ok &= wait_geq(p, h2d_slot(p, src / V, d.chunk), p.host_seq, 0xFFFFFCu);
   }
   return __all_sync(0xFFFFFFFFu, ok);
 }
@@ -548,6 +562,10 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
         dev::st_relaxed_sys(ready_slot(p, dst, q, opi), cur_epoch());
     }
   }
+  else if (p.host_seq && lane == 0) {  // last stage: chunk c is final here -> the D2H stream may copy it
+    dev::fence_acq_rel_sys();
+    dev::st_relaxed_sys(&p.d2h_flags[d.chunk], p.host_seq);
+  }
   if (p.trace && lane == 0) p.trace[2 * opi + 1] = dev::globaltimer();
   __syncwarp();
 }
@@ -627,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           // ring step flags are per absolute CTA index gi: each CTA's slot then
           // sees its ops in order (monotone), and CTA gi of the left neighbour
           // has the same window index li for this op (identical windows).
-          if (u == 0 ? (d.stage > 0 && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
+          if (u == 0 ? ((d.stage > 0 || p.host_seq) && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
             stop = true;
             break;
           }
@@ -720,12 +738,15 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       const int k = d.dim;
       int li, wn;
       if (!op_member(d, gi, gn, li, wn)) continue;
-      if (d.stage > 0) {  // own and dim-k peers' previous stage of this chunk
+      if (d.stage > 0 || p.host_seq) {  // own and dim-k peers' previous stage (or host copy) of this chunk
         const int pk = p.size[k];
         for (int t = tid; t < V * pk; t += blockDim.x) {
           const int q = q0 + t / pk;
           const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
-          ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
+          if (d.stage > 0)
+            ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
+          else
+            ok &= wait_geq(p, h2d_slot(p, src / V, d.chunk), p.host_seq, 0xFFFFFCu);
         }
         ok = __syncthreads_and(ok);
         if (!ok) break;
@@ -753,6 +774,13 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
   __syncthreads();
   for (int i = tid; i < V * P; i += blockDim.x) dev::st_release_sys(exit_slot(p, i % P, q0 + i / P), cur_epoch());
   for (int i = tid; i < V * P; i += blockDim.x) wait_geq(p, exit_slot(p, q0 + i / P, i % P), cur_epoch(), 0xFFFFFDu);
+  // host-buffer mode: every chunk's d2h flag is set by now; set them again so a
+  // D2H stream waiting on them is released even when the kernel aborted
+  // (the error is latched and reported by the next call)
+  if (p.host_seq) {
+    __threadfence_system();
+    for (int i = tid; i < p.C; i += blockDim.x) dev::st_relaxed_sys(&p.d2h_flags[i], p.host_seq);
+  }
   // every CTA has read the epoch (all counted in done_cnt): advance it for the next launch
   __syncthreads();
   if (tid == 0) *(volatile uint32_t*)p.epoch_ctr = cur_epoch();

@@ -345,21 +345,35 @@ def test_trace_follows_enforced_order():
         comm.close()
 
 
-def test_host_buffer_entry_point():
-    topo = th.Topology((2, 2), (1, 1))
-    C_ = 4
-    N = 4 * C_ * 1024
+@pytest.mark.parametrize("sizes,bw,C_,dtype", [((2, 2), (1, 1), 4, "i32"), ((2, 2, 2), (1, 1, 1), 16, "f32"),
+                                               ((4, 2), (2, 1), 8, "i32"), ((2, 2, 2), (4, 2, 1), 64, "f32")])
+def test_host_buffer_entry_point(sizes, bw, C_, dtype):
+    """themis_allreduce_host streams chunks host -> device -> host around the
+    kernel (h2d / d2h flags); three back-to-back calls with fresh inputs, each
+    checked: int32 exact, fp32 bit-exact vs the oracle's schedule."""
+    topo = th.Topology(sizes, bw)
+    P = topo.P
+    N = P * C_ * (RAGGED[dtype] // 4 + 3)
     comm = th.Comm(topo, N * 4)
+    comm.set_timeout(10.0)
     plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm)
     try:
-        xs = host_inputs(4, N, "i32")
-        hin = torch.from_numpy(np.concatenate(xs)).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
-        th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "i32", plan)
+        outs = []
+        for it in range(3):
+            xs = host_inputs(P, N, dtype, seed=1000 + it)
+            hin = torch.from_numpy(np.concatenate(xs)).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, dtype, plan)
+            outs.append((xs, hin, hout))
         torch.cuda.synchronize()
-        want = O.allreduce_definition(xs, "i32")
-        for r in range(4):
-            assert np.array_equal(hout.numpy()[r * N:(r + 1) * N], want)
+        comm.status()
+        for xs, _, hout in outs:
+            if dtype == "i32":
+                want = [O.allreduce_definition(xs, "i32")] * P
+            else:
+                want = O.run_schedule(xs, oracle_sched(sizes, bw, S.AR, N * 4, C_, th.THEMIS), dtype)
+            for r in range(P):
+                assert np.array_equal(hout.numpy()[r * N:(r + 1) * N].view(np.uint8), want[r].view(np.uint8)), r
     finally:
         plan.close()
         comm.close()
