@@ -101,6 +101,12 @@ typedef struct {
                               k > 1: the pre-simulation runs k parallel servers of BW_K/k per
                               dim and assigns each op a server; bound plans
                               run server s's ops on the s-th slice of the dim's CTAs */
+  int32_t reserved;        /* must be 0 */
+  uint64_t chunk_release_ns; /* 0 (the paper's model): every chunk is ready at t = 0.
+                              r > 0: chunk c's first stage becomes ready at (c+1)*r ns in
+                              the pre-simulation — chunks streamed in from the host at
+                              one per r ns (themis_allreduce_host), so the enforced
+                              per-dim order drains early chunks while later ones arrive */
 } themis_plan_req_t;
 
 /* Summary of a plan.  Times in units of 1/time_scale ns, volumes in units of

@@ -90,7 +90,7 @@ def _key(policy: str, op: Op, ready):
 
 
 def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
-             enforced=None, servers: int = 1, enforced_server=None) -> RunMetrics:
+             enforced=None, servers: int = 1, enforced_server=None, release=0) -> RunMetrics:
     """Run the chunk pipelines.  With `enforced` (per-dim [(chunk, stage)]),
     each dim must start its ops in exactly that order (the runtime contract,
     PAPER.md:530); raises RuntimeError on deadlock.
@@ -100,15 +100,20 @@ def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
     servers with BW_K / servers each (an op takes volume*B_K*servers); idle
     servers, in index order, each start the best ready op; m.server records
     which server ran each op.  With enforced_server ((chunk, stage) ->
-    server), each server replays its own sub-list of `enforced` in order."""
+    server), each server replays its own sub-list of `enforced` in order.
+
+    release > 0 (extension, R26): chunk c's first stage becomes
+    ready at (c+1)*release instead of 0 (chunks streamed in from the host);
+    arrivals at t are processed after the completions at t and before the
+    starts."""
     topo = sched.topo
     D = topo.D
     ops = chunk_ops(sched, charge_latency, servers)
     total = sum(len(o) for o in ops)
     queue = [dict() for _ in range(D)]          # (chunk, stage) -> ready time
-    for c, o in enumerate(ops):
-        if o:
-            queue[o[0].dim][(c, 0)] = Fraction(0)
+    release = Fraction(release)
+    arrivals = [(release * (c + 1), c) for c, o in enumerate(ops) if o]   # ready time of stage 0
+    nxt_arrival = 0
     running = [[None] * servers for _ in range(D)]   # (chunk, stage, end)
     lists = None
     if enforced is not None:
@@ -122,6 +127,10 @@ def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
     t = Fraction(0)
     done = 0
     while done < total:
+        while nxt_arrival < len(arrivals) and arrivals[nxt_arrival][0] <= t:   # arrivals at time t
+            r, c = arrivals[nxt_arrival]
+            queue[ops[c][0].dim][(c, 0)] = r
+            nxt_arrival += 1
         for k in range(D):                      # starts at time t
             for sv in range(servers):
                 if running[k][sv] is not None or not queue[k]:
@@ -146,6 +155,8 @@ def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
                 m.busy[k] += op.duration / servers
                 m.volume[k] += op.volume
         ends = [r[2] for rk in running for r in rk if r is not None]
+        if nxt_arrival < len(arrivals):
+            ends.append(arrivals[nxt_arrival][0])
         if not ends:
             raise RuntimeError("deadlock: no op running and unfinished ops remain")
         t = min(ends)

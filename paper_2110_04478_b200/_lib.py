@@ -36,7 +36,7 @@ class Topology_t(C.Structure):
 class PlanReq_t(C.Structure):
     _fields_ = [("coll", C.c_int32), ("policy", C.c_int32), ("intra", C.c_int32), ("n_chunks", C.c_int32),
                 ("bytes", C.c_uint64), ("threshold_div", C.c_int32), ("charge_latency", C.c_int32),
-                ("concurrency", C.c_int32)]
+                ("concurrency", C.c_int32), ("reserved", C.c_int32), ("chunk_release_ns", C.c_uint64)]
 
 
 class PlanInfo_t(C.Structure):

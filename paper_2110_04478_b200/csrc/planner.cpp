@@ -76,6 +76,8 @@ themis_status_t validate(const themis_topology_t* t, const themis_plan_req_t* r)
   if (r->bytes == 0) return fail(THEMIS_ERR_INVALID_ARG, "bytes must be > 0");
   if (r->threshold_div < 1) return fail(THEMIS_ERR_INVALID_ARG, "threshold_div must be >= 1");
   if (r->concurrency < 0 || r->concurrency > 64) return fail(THEMIS_ERR_INVALID_ARG, "concurrency must be 0..64");
+  if (r->reserved != 0) return fail(THEMIS_ERR_INVALID_ARG, "reserved must be 0");
+  if (r->chunk_release_ns > (1ull << 40)) return fail(THEMIS_ERR_INVALID_ARG, "chunk_release_ns must be <= 2^40");
   return THEMIS_OK;
 }
 
@@ -277,7 +279,13 @@ struct Planner {
     const int total = C * NS;
     struct Ready { int chunk, stage; u128 t; };
     std::vector<std::vector<Ready>> q(D);
-    for (int c = 0; c < C; ++c) q[pl.ops[(size_t)c * NS].dim].push_back({c, 0, 0});
+    // chunk c's first stage is ready at 0, or at (c+1) * release with host streaming
+    const u128 release = (u128)pl.req.chunk_release_ns * pl.time_scale;
+    int released = 0;
+    auto release_until = [&](u128 now) {
+      for (; released < C && (release == 0 || (u128)(released + 1) * release <= now); ++released)
+        q[pl.ops[(size_t)released * NS].dim].push_back({released, 0, release * (u128)(released + 1)});
+    };
     // k parallel servers per dim (concurrency <= 1: one)
     const int SV = std::max(1, pl.req.concurrency);
     struct Run { bool on; int chunk, stage; u128 end; };
@@ -308,6 +316,7 @@ struct Planner {
     u128 t = 0;
     int done = 0;
     while (done < total) {
+      release_until(t);  // after the completions at t, before the starts at t (R11)
       for (int k = 0; k < D; ++k)
         for (int sv = 0; sv < SV; ++sv) {
           Run& rk = run[(size_t)k * SV + sv];
@@ -332,7 +341,11 @@ struct Planner {
           nt = rk.end;
           any = true;
         }
-      t = nt;  // always some op running: chains make progress
+      if (released < C && (!any || (u128)(released + 1) * release < nt)) {  // next arrival first
+        nt = (u128)(released + 1) * release;
+        any = true;
+      }
+      t = nt;  // some op running or a chunk still to arrive: progress
       for (int k = 0; k < D; ++k)
         for (int sv = 0; sv < SV; ++sv) {
           Run& rk = run[(size_t)k * SV + sv];
@@ -365,7 +378,10 @@ struct Planner {
   void hash() {
     uint64_t h = 1469598103934665603ull;
     h = fnv(h, &pl.topo, sizeof(pl.topo));
-    h = fnv(h, &pl.req, sizeof(pl.req));
+    const themis_plan_req_t& r = pl.req;  // field by field: struct padding is not hashed
+    const int64_t f[] = {r.coll, r.policy, r.intra, r.n_chunks, (int64_t)r.bytes, r.threshold_div,
+                         r.charge_latency, r.concurrency, (int64_t)r.chunk_release_ns};
+    h = fnv(h, f, sizeof(f));
     h = fnv(h, pl.rs.data(), pl.rs.size());
     h = fnv(h, pl.ag.data(), pl.ag.size());
     for (auto& v : pl.dim_ops) h = fnv(h, v.data(), v.size() * sizeof(uint32_t));

@@ -59,8 +59,10 @@ class Topology:
 
 
 def themis_plan(topo: Topology, coll: int, nbytes: int, n_chunks: int, policy: int = THEMIS, intra: int = SCF,
-                threshold_div: int = 16, charge_latency: bool = False, concurrency: int = 1) -> C.c_void_p:
-    req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency), concurrency)
+                threshold_div: int = 16, charge_latency: bool = False, concurrency: int = 1,
+                chunk_release_ns: int = 0) -> C.c_void_p:
+    req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency), concurrency, 0,
+                    int(chunk_release_ns))
     out = C.c_void_p()
     tc = topo.to_c()
     check(lib().themis_plan(C.byref(tc), C.byref(req), C.byref(out)))
@@ -72,9 +74,10 @@ class Plan:
 
     def __init__(self, topo: Topology, coll: int = ALLREDUCE, nbytes: int = 0, n_chunks: int = 64,
                  policy: int = THEMIS, intra: int = SCF, threshold_div: int = 16, charge_latency: bool = False,
-                 rs_orders=None, ag_orders=None, concurrency: int = 1):
+                 rs_orders=None, ag_orders=None, concurrency: int = 1, chunk_release_ns: int = 0):
         """rs_orders / ag_orders (C x D, 0-based): caller-given per-chunk
-        orders (themis_plan_custom) instead of Algorithm 1."""
+        orders (themis_plan_custom) instead of Algorithm 1.  chunk_release_ns:
+        chunk c arrives at (c+1) * r ns in the pre-simulation (host streaming)."""
         self.topo = topo
         self.coll = coll
         self.nbytes = int(nbytes)
@@ -83,10 +86,10 @@ class Plan:
         self.intra = intra
         if rs_orders is None and ag_orders is None:
             self.h = themis_plan(topo, coll, nbytes, n_chunks, policy, intra, threshold_div, charge_latency,
-                                 concurrency)
+                                 concurrency, chunk_release_ns)
         else:
             req = PlanReq_t(coll, policy, intra, n_chunks, int(nbytes), threshold_div, int(charge_latency),
-                            concurrency)
+                            concurrency, 0, int(chunk_release_ns))
             rs = None if rs_orders is None else np.ascontiguousarray(np.asarray(rs_orders, np.uint8).reshape(-1))
             ag = None if ag_orders is None else np.ascontiguousarray(np.asarray(ag_orders, np.uint8).reshape(-1))
             out = C.c_void_p()

@@ -345,9 +345,11 @@ def test_trace_follows_enforced_order():
         comm.close()
 
 
-@pytest.mark.parametrize("sizes,bw,C_,dtype", [((2, 2), (1, 1), 4, "i32"), ((2, 2, 2), (1, 1, 1), 16, "f32"),
-                                               ((4, 2), (2, 1), 8, "i32"), ((2, 2, 2), (4, 2, 1), 64, "f32")])
-def test_host_buffer_entry_point(sizes, bw, C_, dtype):
+@pytest.mark.parametrize("sizes,bw,C_,dtype,release", [((2, 2), (1, 1), 4, "i32", 0),
+                                                       ((2, 2, 2), (1, 1, 1), 16, "f32", 0),
+                                                       ((4, 2), (2, 1), 8, "i32", 0),
+                                                       ((2, 2, 2), (4000, 2000, 1000), 64, "f32", 20_000)])
+def test_host_buffer_entry_point(sizes, bw, C_, dtype, release):
     """themis_allreduce_host streams chunks host -> device -> host around the
     kernel (h2d / d2h flags); three back-to-back calls with fresh inputs, each
     checked: int32 exact, fp32 bit-exact vs the oracle's schedule."""
@@ -356,7 +358,7 @@ def test_host_buffer_entry_point(sizes, bw, C_, dtype):
     N = P * C_ * (RAGGED[dtype] // 4 + 3)
     comm = th.Comm(topo, N * 4)
     comm.set_timeout(10.0)
-    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_).bind(comm)
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_, chunk_release_ns=release).bind(comm)
     try:
         outs = []
         for it in range(3):

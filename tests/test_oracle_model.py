@@ -456,3 +456,22 @@ def test_choose_chunks_pipelining_without_latency():
     assert one.makespan == (F(S_, 2) + F(S_, 4) + F(S_, 4) + F(S_, 2)) / 100   # chain of 4 stages, nothing overlaps
     assert C > 1 and m.makespan < one.makespan
     assert m.makespan >= E.ideal_time(sched)
+
+
+def test_release_streaming_closed_form():
+    """R26: when chunks arrive slower than one chunk's whole chain takes, each
+    chunk runs alone: makespan = C*r + (sum of the last chunk's stage times),
+    and stage 0 of chunk c starts exactly at its arrival (c+1)*r."""
+    from fractions import Fraction as F
+    from oracle import engine as E, scheduler as S, topology as T
+    t = T.Topology.make((2, 2, 2), [F(100), F(50), F(25)])
+    S_, C = 1 << 20, 8
+    sched = S.schedule_collective(t, S.AR, S_, C, S.BASELINE)
+    chain = sum(op.duration for op in E.chunk_ops(sched)[C - 1])
+    r = chain + 1
+    m = E.simulate(sched, E.FIFO, release=r)
+    assert m.makespan == C * r + chain
+    for c in range(C):
+        assert m.start[(c, 0)] == (c + 1) * r
+    # release = 0 is the paper's model (everything ready at t = 0)
+    assert E.simulate(sched, E.FIFO, release=0).makespan == E.simulate(sched, E.FIFO).makespan

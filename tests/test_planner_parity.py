@@ -28,11 +28,11 @@ def make_pair(sizes, bw_mbps, kinds=None, lat=None):
     return o, g
 
 
-def compare(o_topo, g_topo, coll, nbytes, C, policy, intra, div=16, charge=False):
+def compare(o_topo, g_topo, coll, nbytes, C, policy, intra, div=16, charge=False, release=0):
     sched = S.schedule_collective(o_topo, coll, nbytes, C, policy, div)
-    m = E.simulate(sched, intra, charge_latency=charge)
+    m = E.simulate(sched, intra, charge_latency=charge, release=release)
     plan = th.Plan(g_topo, COLLS[coll], nbytes, C, th.THEMIS if policy == S.THEMIS else th.BASELINE,
-                   INTRA[intra], div, charge)
+                   INTRA[intra], div, charge, chunk_release_ns=release)
     try:
         info = plan.info
         ts, bs = info["time_scale"], info["byte_scale"]
@@ -262,3 +262,18 @@ def test_auto_chunks_alignment_error():
     with pytest.raises(th.ThemisError) as e:
         th.Plan(g, th.ALLREDUCE, 4 * 16 + 8, th.AUTO_CHUNKS)
     assert e.value.status == 2          # THEMIS_ERR_ALIGNMENT
+
+
+@pytest.mark.parametrize("release", [1, 37, 2000, 250_000])
+def test_chunk_release_parity(release):
+    """Host streaming (R26): chunk c ready at (c+1)*release ns — per-dim order
+    and every start/end time bit-exact against the oracle, both policies,
+    with and without per-op latency, including ties between arrivals and
+    completions."""
+    o, g = make_pair((2, 2, 2), (100000, 100000, 100000), lat=[500, 700, 900])
+    for pol in (S.BASELINE, S.THEMIS):
+        for ip in (E.SCF, E.FIFO):
+            for charge in (False, True):
+                compare(o, g, S.AR, 64 << 20, 16, pol, ip, charge=charge, release=release)
+    o, g = make_pair((4, 2), (200000, 50000))
+    compare(o, g, S.AR, 16 << 20, 8, S.THEMIS, E.SCF, release=release)
