@@ -328,7 +328,8 @@ def run_themis(a):
         comm.rank_view(0, probe, "f32").copy_(hin[:probe], non_blocking=True)
         d1.record()
         torch.cuda.synchronize()
-        h2d_gbs = probe * 4 / (d0.elapsed_time(d1) / 1e3) / 1e9
+        # the slowest GPU's rate: every rank must build the identical plan
+        h2d_gbs = -max_over_ranks(-(probe * 4 / (d0.elapsed_time(d1) / 1e3) / 1e9), group, dev)
         release_ns = int(V * S / a.chunks / h2d_gbs)
         bw_abs = paced_bw(ratio, max(24.0, busbw(t_main)))
         try:
