@@ -330,6 +330,24 @@ def run_themis(a):
         torch.cuda.synchronize()
         # the slowest GPU's rate: every rank must build the identical plan
         h2d_gbs = -max_over_ranks(-(probe * 4 / (d0.elapsed_time(d1) / 1e3) / 1e9), group, dev)
+        # PCIe bound of the e2e step: both directions at once (per-direction rate)
+        sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        scratch = torch.empty(probe, dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        d0.record()
+        sa.wait_event(d0)
+        sb.wait_event(d0)
+        with torch.cuda.stream(sa):
+            comm.rank_view(0, probe, "f32").copy_(hin[:probe], non_blocking=True)
+        with torch.cuda.stream(sb):
+            hout_probe = torch.empty(probe, dtype=torch.float32, pin_memory=True)
+            hout_probe.copy_(scratch, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(sa)
+        torch.cuda.current_stream().wait_stream(sb)
+        d1.record()
+        torch.cuda.synchronize()
+        duplex_gbs = -max_over_ranks(-(probe * 4 / (d0.elapsed_time(d1) / 1e3) / 1e9), group, dev)
+        del scratch, hout_probe
         release_ns = int(V * S / a.chunks / h2d_gbs)
         bw_abs = paced_bw(ratio, max(24.0, busbw(t_main)))
         try:
@@ -354,6 +372,9 @@ def run_themis(a):
         comm.status()
         e2e = {"value": round(busbw(te), 2), "unit": "GB/s", "h2d_bytes_per_step": V * S, "d2h_bytes_per_step": V * S,
                "ms_per_step": round(te * 1e3, 3), "h2d_gbs_measured": round(h2d_gbs, 1),
+               "pcie_duplex_gbs_measured": round(duplex_gbs, 1),
+               "pcie_bound_ms": round(V * S / duplex_gbs / 1e6, 3),
+               "frac_of_pcie_bound": round(V * S / duplex_gbs / 1e9 / te, 3),
                "chunk_release_ns": release_ns,
                "note": "themis_allreduce_host: chunk-streamed H2D -> collective -> D2H (pinned host buffers)"}
         hplan.close()
