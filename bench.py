@@ -333,6 +333,7 @@ def run_themis(a):
         # PCIe bound of the e2e step: both directions at once (per-direction rate)
         sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
         scratch = torch.empty(probe, dtype=torch.float32, device=dev)
+        hout_probe = torch.empty(probe, dtype=torch.float32, pin_memory=True)
         torch.cuda.synchronize()
         d0.record()
         sa.wait_event(d0)
@@ -340,7 +341,6 @@ def run_themis(a):
         with torch.cuda.stream(sa):
             comm.rank_view(0, probe, "f32").copy_(hin[:probe], non_blocking=True)
         with torch.cuda.stream(sb):
-            hout_probe = torch.empty(probe, dtype=torch.float32, pin_memory=True)
             hout_probe.copy_(scratch, non_blocking=True)
         torch.cuda.current_stream().wait_stream(sa)
         torch.cuda.current_stream().wait_stream(sb)
