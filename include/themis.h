@@ -202,10 +202,12 @@ themis_status_t themis_comm_status(themis_comm_t* comm);
  * into a shared-memory ring + warp-specialised reduction; 0 = per-thread
  * 16-byte LDG/STG.  Env THEMIS_COPY_ENGINE=ldg|tma sets the default. */
 themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
-/* Bandwidth emulation by pacing (TMA engine): when on, every CTA of dim k's
- * group pulls peer bytes no faster than V * bw_mbps[k] / ctas[k], so dim k's
- * per-rank rate is capped at the bound plan topology's absolute bw_mbps[k]
- * (B_K = 1/BW_K).  Off (default): only the CTA caps limit it. */
+/* Bandwidth emulation by pacing (TMA engine): when on, dim k is one emulated
+ * link of V * bw_mbps[k] shared by all CTAs, ops, windows and servers of its
+ * group — each tile's peer bytes reserve the link (token bucket, no banked
+ * credit while idle) — so dim k's per-rank rate is capped at the bound plan
+ * topology's absolute bw_mbps[k] (B_K = 1/BW_K).  Off
+ * (default): only the CTA caps limit it. */
 themis_status_t themis_comm_set_pacing(themis_comm_t* comm, int32_t on);
 /* TMA ring per CTA: `stages` slots of `stage_bytes` (bytes in flight per CTA
  * = stages x stage_bytes <= 192 KiB); defaults 6 x 32 KiB, env THEMIS_STAGES /
@@ -221,6 +223,13 @@ themis_status_t themis_comm_set_stage_bytes(themis_comm_t* comm, int32_t stage_b
  * dimension as in the pre-simulation.  Takes effect at the next
  * themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t bytes);
+/* Window placement for min_cta_bytes > 0: rotate = 1 (default, env
+ * THEMIS_WINDOW_ROTATE) consecutive ops of a dimension take consecutive CTA
+ * windows (several small ops in flight); rotate = 0: every narrow op starts at
+ * the group's first CTA, so ops stay one at a time in the enforced order but a
+ * small op occupies (and synchronises) only the CTAs it needs.  Takes effect at
+ * the next themis_plan_bind.  Errors: INVALID_ARG. */
+themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rotate);
 /* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */
 themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
 /* Trace: when enabled, each dim group records %globaltimer start/end of every

@@ -72,7 +72,7 @@ struct themis_comm {
   char* heap[THEMIS_MAX_GPUS] = {};
   uint64_t heap_bytes = 0, vrank_stride = 0, sig_bytes = 0;
   uint32_t* opcnt = nullptr;
-  unsigned long long* op_t0 = nullptr;
+  unsigned long long* dim_clock = nullptr;  // [THEMIS_MAX_DIMS] paced links (pacing)
   uint32_t* done_cnt = nullptr;
   uint32_t* abort_flag = nullptr;
   uint32_t* epoch_ctr = nullptr;  // device-resident collective epoch (graph-replay safe)
@@ -85,6 +85,7 @@ struct themis_comm {
   int stage_bytes = kStageBytes;  // bytes per ring stage (themis_comm_set_stage_bytes)
   int ag_rr = 0;                  // direct-AG tile shape (env THEMIS_AG_RR, experiment)
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
+  int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -181,8 +182,8 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
       (e = cudaMalloc(&c->opcnt, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
-      (e = cudaMalloc(&c->op_t0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
-      (e = cudaMemset(c->op_t0, 0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
+      (e = cudaMalloc(&c->dim_clock, sizeof(unsigned long long) * THEMIS_MAX_DIMS)) != cudaSuccess ||
+      (e = cudaMemset(c->dim_clock, 0, sizeof(unsigned long long) * THEMIS_MAX_DIMS)) != cudaSuccess ||
       (e = cudaMemset(c->opcnt, 0, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
       (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
@@ -209,6 +210,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if (const char* env = getenv("THEMIS_STAGES"))
     c->stages = std::max(1, std::min(std::min(kStages, kStages * kStageBytes / c->stage_bytes), atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
+  if (const char* env = getenv("THEMIS_WINDOW_ROTATE")) c->window_rotate = atoi(env) != 0;
   c->max_blocks = nb * c->num_sms;
   *out = c;
   return THEMIS_OK;
@@ -226,7 +228,7 @@ extern "C" void themis_comm_free(themis_comm_t* c) {
     cudaFree(c->d2h_flags);
   }
   cudaFree(c->opcnt);
-  cudaFree(c->op_t0);
+  cudaFree(c->dim_clock);
   cudaFree(c->trace);
   cudaFreeHost(c->herr_host);
   delete c;
@@ -244,6 +246,11 @@ extern "C" themis_status_t themis_comm_status(themis_comm_t* c) {
 extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engine) {
   if (!c || engine < 0 || engine > 1) return fail(THEMIS_ERR_INVALID_ARG, "engine must be 0 (LDG) or 1 (TMA)");
   c->engine = engine;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_window_rotation(themis_comm_t* c, int32_t rotate) {
+  if (!c || rotate < 0 || rotate > 1) return fail(THEMIS_ERR_INVALID_ARG, "rotate must be 0 or 1");
+  c->window_rotate = rotate;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint64_t bytes) {
@@ -407,7 +414,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
         w = std::max(1, std::min(n[k], w));
         d.width = w;
         d.offset = off;
-        off = (off + w) % n[k];
+        off = c->window_rotate ? (off + w) % n[k] : 0;
       }
     }
   }
@@ -503,7 +510,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.elem_size = esz;
   kp.epoch_ctr = c->epoch_ctr;
   kp.opcnt = c->opcnt;
-  kp.op_t0 = c->op_t0;
+  kp.dim_clock = c->dim_clock;
   kp.done_cnt = c->done_cnt;
   kp.abort_flag = c->abort_flag;
   kp.herr = c->herr_dev;
@@ -522,9 +529,8 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.ag_rr = c->ag_rr;
   kp.host_seq = host_seq;
   kp.d2h_flags = c->d2h_flags;
-  for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
-    kp.pace_ns_per_byte[k] =
-        c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
+  for (int k = 0; k < pl->D; ++k)  // ns per peer byte of dim k's link = 1 / (V * bw_k[bytes/ns])
+    kp.pace_ns_per_byte[k] = c->pacing ? (float)(1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
 
   void* args[] = {&kp};
   if (!c->engine)

@@ -267,6 +267,10 @@ class Comm:
         """Op-window sizing: small ops run on fewer CTAs, several in flight."""
         check(lib().themis_comm_set_min_cta_bytes(self.h, int(nbytes)))
 
+    def set_window_rotation(self, rotate: bool) -> None:
+        """Op windows: consecutive windows (True) or every narrow op from CTA 0."""
+        check(lib().themis_comm_set_window_rotation(self.h, int(rotate)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
 

@@ -53,6 +53,9 @@ def main():
     ap.add_argument("--paced", action="store_true")
     ap.add_argument("--pace-gbs", type=float, default=0)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--min-cta-kb", type=int, default=0, help="op windows: min bytes per CTA (KiB), 0 = full width")
+    ap.add_argument("--rotate", type=int, default=1, help="op windows: consecutive windows (1) or from CTA 0 (0)")
+    ap.add_argument("--sizes-mib", default="1,4,16,64,256")
     a = ap.parse_args()
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     out_fd = os.dup(1)
@@ -74,6 +77,8 @@ def main():
     comm.set_timeout(60.0)
     comm.set_stages(6 if ncross == 0 else (3 if ncross == D else 4))
     comm.set_pacing(a.paced)
+    comm.set_min_cta_bytes(a.min_cta_kb * 1024)
+    comm.set_window_rotation(bool(a.rotate))
 
     def emit(obj):
         if rank == 0:
@@ -150,6 +155,7 @@ def main():
     bw_cal = tuple(max(1, int(round(x / 5))) * 5000 for x in bw_meas)
     lat_cal = tuple(int(round(x)) for x in A)
     emit({"calibration": True, "n_gpus": world, "ranks_per_gpu": V, "ratio": a.ratio,
+          "min_cta_kb": a.min_cta_kb, "rotate": a.rotate,
           "mode": "paced" if a.paced else "caps", "ctas_per_dim": ctas, "A_ns": [round(x, 1) for x in A],
           "handoff_ns": round(handoff, 1), "min_collective_us": round(t_min / 1e3, 2),
           "bw_gbs_measured": [round(x, 1) for x in bw_meas], "big_collective_ms": round(t_big / 1e6, 3),
@@ -157,7 +163,7 @@ def main():
 
     # 3. validation: model vs measured; latency-aware Themis vs plain Themis vs baseline
     cal = th.Topology(sizes, bw_cal, None, lat_cal)
-    for mib in (1, 4, 16, 64, 256):
+    for mib in [int(x) for x in a.sizes_mib.split(",")]:
         fixed = {}
         for C in (4, 16, 64):
             nbytes = mib << 20

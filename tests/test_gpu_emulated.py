@@ -41,7 +41,7 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
-             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1):
+             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1, rotate=1):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
@@ -50,6 +50,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_engine(engine)
     comm.set_timeout(10.0)
     comm.set_min_cta_bytes(min_cta_bytes)
+    comm.set_window_rotation(bool(rotate))
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra, concurrency=concurrency).bind(comm, ctas)
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
@@ -143,8 +144,9 @@ def test_op_windows_several_ops_in_flight(sizes, kinds):
     a dimension in flight — results unchanged (int32 exact, f32 bit-exact)."""
     bw = (1,) * len(sizes)
     for mcb in (4096, 65536):
-        check_ar(sizes, bw, "i32", 64, 516, kinds=kinds, min_cta_bytes=mcb, ctas=[12] * len(sizes))
-        check_ar(sizes, bw, "f32", 16, 2052, kinds=kinds, min_cta_bytes=mcb, dist="wide")
+        for rot in (1, 0):          # consecutive windows / every narrow op from CTA 0
+            check_ar(sizes, bw, "i32", 64, 516, kinds=kinds, min_cta_bytes=mcb, ctas=[12] * len(sizes), rotate=rot)
+            check_ar(sizes, bw, "f32", 16, 2052, kinds=kinds, min_cta_bytes=mcb, dist="wide", rotate=rot)
 
 
 @pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), (Dk, Dk, Dk)), ((4, 2), (R, Dk)), ((3, 2, 2), (R, Dk, R))])
