@@ -202,12 +202,12 @@ themis_status_t themis_comm_status(themis_comm_t* comm);
  * into a shared-memory ring + warp-specialised reduction; 0 = per-thread
  * 16-byte LDG/STG.  Env THEMIS_COPY_ENGINE=ldg|tma sets the default. */
 themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
-/* Bandwidth emulation by pacing (TMA engine): when on, dim k is one emulated
- * link of V * bw_mbps[k] shared by all CTAs, ops, windows and servers of its
- * group — each tile's peer bytes reserve the link (token bucket, no banked
- * credit while idle) — so dim k's per-rank rate is capped at the bound plan
- * topology's absolute bw_mbps[k] (B_K = 1/BW_K).  Off
- * (default): only the CTA caps limit it. */
+/* Bandwidth emulation by pacing (TMA engine): when on, every CTA of dim k's
+ * group pulls peer bytes no faster than V * bw_mbps[k] / ctas[k] (absolute
+ * due times from a group-shared op origin), so dim k's per-rank rate is capped
+ * at the bound plan topology's absolute bw_mbps[k] (B_K =
+ * 1/BW_K); a lone narrow op (op windows without rotation) on w CTAs paces at
+ * V * bw_mbps[k] / w per CTA.  Off (default): only the CTA caps limit it. */
 themis_status_t themis_comm_set_pacing(themis_comm_t* comm, int32_t on);
 /* TMA ring per CTA: `stages` slots of `stage_bytes` (bytes in flight per CTA
  * = stages x stage_bytes <= 192 KiB); defaults 6 x 32 KiB, env THEMIS_STAGES /

@@ -72,7 +72,7 @@ struct themis_comm {
   char* heap[THEMIS_MAX_GPUS] = {};
   uint64_t heap_bytes = 0, vrank_stride = 0, sig_bytes = 0;
   uint32_t* opcnt = nullptr;
-  unsigned long long* dim_clock = nullptr;  // [THEMIS_MAX_DIMS] paced links (pacing)
+  unsigned long long* op_t0 = nullptr;
   uint32_t* done_cnt = nullptr;
   uint32_t* abort_flag = nullptr;
   uint32_t* epoch_ctr = nullptr;  // device-resident collective epoch (graph-replay safe)
@@ -182,8 +182,8 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
       (e = cudaMalloc(&c->opcnt, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
-      (e = cudaMalloc(&c->dim_clock, sizeof(unsigned long long) * THEMIS_MAX_DIMS)) != cudaSuccess ||
-      (e = cudaMemset(c->dim_clock, 0, sizeof(unsigned long long) * THEMIS_MAX_DIMS)) != cudaSuccess ||
+      (e = cudaMalloc(&c->op_t0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
+      (e = cudaMemset(c->op_t0, 0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->opcnt, 0, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
       (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
@@ -228,7 +228,7 @@ extern "C" void themis_comm_free(themis_comm_t* c) {
     cudaFree(c->d2h_flags);
   }
   cudaFree(c->opcnt);
-  cudaFree(c->dim_clock);
+  cudaFree(c->op_t0);
   cudaFree(c->trace);
   cudaFreeHost(c->herr_host);
   delete c;
@@ -352,6 +352,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   for (size_t i = 0; i < pl->ops.size(); ++i) {
     const Op& o = pl->ops[i];
     OpDesc d{};
+    d.pace_scale = 1.0f;
     d.chunk = o.chunk;
     d.stage = o.stage;
     d.dim = o.dim;
@@ -414,6 +415,9 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
         w = std::max(1, std::min(n[k], w));
         d.width = w;
         d.offset = off;
+        // a lone narrow op (no rotation: ops one at a time) carries the whole
+        // dim rate on its w CTAs; rotating windows share it per CTA
+        d.pace_scale = c->window_rotate ? 1.0f : (float)w / (float)n[k];
         off = c->window_rotate ? (off + w) % n[k] : 0;
       }
     }
@@ -510,7 +514,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.elem_size = esz;
   kp.epoch_ctr = c->epoch_ctr;
   kp.opcnt = c->opcnt;
-  kp.dim_clock = c->dim_clock;
+  kp.op_t0 = c->op_t0;
   kp.done_cnt = c->done_cnt;
   kp.abort_flag = c->abort_flag;
   kp.herr = c->herr_dev;
@@ -529,8 +533,9 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.ag_rr = c->ag_rr;
   kp.host_seq = host_seq;
   kp.d2h_flags = c->d2h_flags;
-  for (int k = 0; k < pl->D; ++k)  // ns per peer byte of dim k's link = 1 / (V * bw_k[bytes/ns])
-    kp.pace_ns_per_byte[k] = c->pacing ? (float)(1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
+  for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
+    kp.pace_ns_per_byte[k] =
+        c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
 
   void* args[] = {&kp};
   if (!c->engine)

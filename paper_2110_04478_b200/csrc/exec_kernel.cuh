@@ -29,6 +29,7 @@ struct OpDesc {
   int32_t ring;                      // 1: ring algorithm on this dim
   int32_t seq;                       // index of the op in its dim's enforced list
   int32_t width, offset;             // the op runs on CTAs [offset, offset+width) mod c_k of its group
+  float pace_scale;                  // pacing: width / c_k for a lone narrow op (it gets the whole dim rate), else 1
   int32_t nfree;                     // dims whose block digit is free
   int32_t free_size[THEMIS_MAX_DIMS];
   int64_t free_stride[THEMIS_MAX_DIMS];
@@ -52,14 +53,14 @@ struct KParams {
   uint32_t* epoch_ctr;      // device: epoch of the last completed collective on this comm
   unsigned long long plan_hash;  // must be identical on every rank (checked at entry)
   uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
-  unsigned long long* dim_clock;  // [THEMIS_MAX_DIMS] paced link of each dim: when it frees up (globaltimer ns x 4)
+  unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
   uint32_t* done_cnt;
   uint32_t* abort_flag;     // device-local: someone timed out
   uint32_t* herr;           // host-mapped error word
   uint64_t timeout_ns;
   uint64_t* trace;          // [C*NS*2] or null
   uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
-  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // ns per peer byte of dim k's emulated link, V ranks (0 = off)
+  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
@@ -330,33 +331,13 @@ static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + com
 
 __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { return ((uint32_t)p.stage_bytes / nsrc) & ~15u; }
 
-// BW emulation by pacing (a9): dim k is one emulated link of V * BW_K shared by
-// every CTA and op of its group.  A producer reserves the link for a tile's
-// peer bytes (token bucket: the slot starts at max(now, when the link frees
-// up)) and issues the tile at the slot's start, so the dim never exceeds its
-// rate however many CTAs / ops / windows / servers are active, and an idle
-// link does not bank credit.
-// The clock counts quarter nanoseconds (a 16 KiB tile at 640 GB/s is 25.6 ns).
-__device__ __forceinline__ void pace_tile(const KParams& p, int dim, float pace, uint32_t peer_bytes) {
-  unsigned long long* clk = &p.dim_clock[dim];
-  const unsigned long long now = 4ull * dev::globaltimer();
-  const unsigned long long len = (unsigned long long)(4.0f * pace * (float)peer_bytes + 0.5f);
-  unsigned long long old = *(volatile unsigned long long*)clk, seen, start;
-  do {
-    seen = old;
-    start = seen > now ? seen : now;
-    old = atomicCAS(clk, seen, start + len);
-  } while (old != seen);
-  while (4ull * dev::globaltimer() < start) {
-  }
-}
-
 // Producer (one lane): stream this CTA's tiles of one unit into the ring.
 __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
-                                             char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+                                             char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
+                                             uint64_t t_op, double& sent) {
   const int nsrc = unit_nsrc(p, d, mode);
   const uint32_t tile = unit_tile(p, nsrc);
-  const float pace = p.pace_ns_per_byte[d.dim];
+  const float pace = p.pace_ns_per_byte[d.dim] * d.pace_scale;
   const int remote = (mode == U_DIRECT_RS || mode == U_DIRECT_AG_T) ? p.size[d.dim] - 1 : 1;  // peer sources/tile
   const uint64_t pstride = part_stride(p, d.dim);
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
@@ -375,7 +356,12 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
       for (uint64_t pos = a; pos < e; pos += big) {
         const uint32_t bytes = (uint32_t)(e - pos < big ? e - pos : big);
         for (int j = 0; j < nsrc; ++j, ++ctr) {
-          if (pace > 0.f) pace_tile(p, d.dim, pace, bytes);
+          if (pace > 0.f) {
+            const uint64_t due = t_op + (uint64_t)(sent * pace);
+            while (dev::globaltimer() < due) {
+            }
+            sent += (double)bytes;
+          }
           const int s = ctr % p.stages;
           dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
           dev::mbar_expect_tx(&full[s], bytes);
@@ -389,7 +375,12 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
     }
     for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
       const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
-      if (pace > 0.f) pace_tile(p, d.dim, pace, bytes * remote);
+      if (pace > 0.f) {  // absolute due times from the group's op origin
+        const uint64_t due = t_op + (uint64_t)(sent * pace);
+        while (dev::globaltimer() < due) {
+        }
+        sent += (double)bytes * remote;
+      }
       const int s = ctr % p.stages;
       dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
       dev::mbar_expect_tx(&full[s], bytes * nsrc);
@@ -540,6 +531,7 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
     if (last) {
       if (p.tdetail) p.tdetail[6 * opi + 3] = dev::globaltimer();
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
+      p.op_t0[opi] = 0;
     }
   }
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
@@ -647,6 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         int li, wn;
         if (!op_member(d, gi, gn, li, wn)) continue;          // op runs on other CTAs of the group
         if (!unit_has_work(p, d, mode, li, wn)) continue;     // nothing to wait for or move
+        uint64_t t_op = 0;
+        double sent = 0.0;
         bool stop = false;
         for (int u = 0; u < nu && !stop; ++u) {
           // ring step flags are per absolute CTA index gi: each CTA's slot then
@@ -663,8 +657,13 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
                 dev::fence_proxy_async_global();
                 p.tdetail[6 * opi + 5] = dev::globaltimer();
               }
+              if (p.pace_ns_per_byte[d.dim] > 0.f) {  // group-shared pacing origin (first starter wins)
+                const unsigned long long now = dev::globaltimer();
+                const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
+                t_op = prev ? prev : now;
+              }
             }
-            produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr);
+            produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent);
             if (p.tdetail && li == 0 && u + 1 == nu) p.tdetail[6 * opi + 0] = dev::globaltimer();
           }
           __syncwarp();
