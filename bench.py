@@ -168,7 +168,12 @@ def run_themis(a):
         total_ctas = min(sms, 32 * len(SIZES) + 32) if len(SIZES) > 1 else 32
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
-    stages = a.stages or (6 if ncross_ == 0 else (3 if ncross_ == len(SIZES) and len(SIZES) > 1 else 4))
+    # ring depth: 6 when some dims are GPU-local (profiles/r01/stages/: N = 2 / 4
+    # gain 2-4 % over 4); all-NVLink topologies peak lower (calibration above)
+    if ncross_ == len(SIZES):
+        stages = a.stages or (3 if len(SIZES) > 1 else 4)
+    else:
+        stages = a.stages or 6
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
     comm.set_timeout(30.0)

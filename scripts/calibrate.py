@@ -75,7 +75,7 @@ def main():
     big = 1 << 30
     comm = th.Comm(th.Topology(sizes, bw_plan), big, group=group, device=local)
     comm.set_timeout(60.0)
-    comm.set_stages(6 if ncross == 0 else (3 if ncross == D else 4))
+    comm.set_stages(3 if ncross == D else 6)
     comm.set_pacing(a.paced)
     comm.set_min_cta_bytes(a.min_cta_kb * 1024)
     comm.set_window_rotation(bool(a.rotate))
