@@ -46,6 +46,8 @@ class Topology:
         return int(np.prod(self.sizes))
 
     def to_c(self) -> Topology_t:
+        if not 1 <= self.D <= MAX_DIMS:
+            raise ThemisError(1, f"ndims must be 1..{MAX_DIMS}")
         t = Topology_t()
         t.ndims = self.D
         kinds = self.kinds or (DIRECT,) * self.D
@@ -313,6 +315,8 @@ class Comm:
         n = ts[0].numel()
         if any(t.numel() != n or t.dtype != ts[0].dtype or t.device != self.device for t in ts):
             raise ValueError("tensors must share numel, dtype and this comm's device")
+        if n == 0:                                   # nothing to reduce (every rank must agree: same numel)
+            return tensors
         g = self.P * (n_chunks or AUTO_MAX_CHUNKS) * (16 // ELEM_SIZE[dt])   # 0 = auto: every candidate fits
         count = max(g, (n + g - 1) // g * g)
         nbytes = count * ELEM_SIZE[dt]

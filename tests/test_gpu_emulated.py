@@ -457,3 +457,24 @@ def test_cuda_graph_capture_and_replay():
     finally:
         plan.close()
         comm.close()
+
+
+def test_max_ranks_and_many_chunks():
+    """Edge sizes on the executor: 64 logical ranks (2^6, the per-comm
+    maximum) in one GPU, and 1024 chunks (THEMIS_MAX_CHUNKS) on 2x2x2 —
+    int32 exact."""
+    check_ar((2,) * 6, (1,) * 6, "i32", 4, 516, ctas=[8] * 6)
+    check_ar((2, 2, 2), (1, 1, 1), "i32", 1024, 8, ctas=[16, 16, 16])
+
+
+def test_tensor_all_reduce_empty():
+    """numel = 0: nothing to reduce, nothing touched, no error."""
+    comm = th.Comm(th.Topology((2, 2), (1, 1)), 1 << 20)
+    try:
+        ts = [torch.empty(0, dtype=torch.float32, device="cuda") for _ in range(4)]
+        comm.all_reduce(ts, n_chunks=4)
+        torch.cuda.synchronize()
+        comm.status()
+        assert all(t.numel() == 0 for t in ts)
+    finally:
+        comm.close()

@@ -277,3 +277,17 @@ def test_chunk_release_parity(release):
                 compare(o, g, S.AR, 64 << 20, 16, pol, ip, charge=charge, release=release)
     o, g = make_pair((4, 2), (200000, 50000))
     compare(o, g, S.AR, 16 << 20, 8, S.THEMIS, E.SCF, release=release)
+
+
+def test_max_dims_and_chunks():
+    """Edge sizes: THEMIS_MAX_DIMS = 8 dims (2^8 ranks) and 1024 chunks
+    (THEMIS_MAX_CHUNKS), both policies, bit-exact against the oracle."""
+    o, g = make_pair((2,) * 8, (8000, 7000, 6000, 5000, 4000, 3000, 2000, 1000))
+    for pol in (S.BASELINE, S.THEMIS):
+        compare(o, g, S.AR, 256 << 20, 8, pol, E.SCF)
+    o, g = make_pair((2, 2, 2), (1000, 1000, 1000))
+    compare(o, g, S.AR, 1 << 30, 1024, S.THEMIS, E.SCF)
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2,) * 9, (1,) * 9), th.ALLREDUCE, 1 << 20, 4)
+    with pytest.raises(th.ThemisError):
+        th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1 << 20, 1025)
