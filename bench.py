@@ -214,6 +214,7 @@ def run_themis(a):
             ts.append(e0.elapsed_time(e1) / 1e3)
         comm.status()
         mean = sum(ts) / len(ts)
+        timed.median = max_over_ranks(sorted(ts)[len(ts) // 2], group, dev)
         return max_over_ranks(mean, group, dev), max_over_ranks(min(ts), group, dev)
 
     busbw = lambda t: 2 * S * (P - 1) / P / t / 1e9
@@ -222,6 +223,7 @@ def run_themis(a):
     clocks = ClockSampler(local)
     with clocks:
         t_main, t_best = timed(main, a.steps, a.warmup)
+        t_median = timed.median
     launches = a.steps * th.launches_per_call()
 
     # Themis vs baseline order under the emulated ratios
@@ -435,6 +437,7 @@ def run_themis(a):
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
                        "aggregate_bus_gbs": round(busbw(t_main) * P, 1),
                        "best_step_bus_gbs": round(busbw(t_best), 2),
+                       "median_step_bus_gbs": round(busbw(t_median), 2),
                        "l2": "inputs refreshed from a pristine copy before every step (>= 1 GiB per GPU written, "
                              "> 126 MB L2); inputs larger than L2"},
             "clocks": clocks.summary(), "gpu_launches": launches, "roofline": roof, "e2e": e2e,
