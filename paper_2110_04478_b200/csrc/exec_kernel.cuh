@@ -112,12 +112,12 @@ __device__ __forceinline__ int ring_peer(const KParams& p, int q, int k, int del
   return q + (((c + delta) % pk + pk) % pk - c) * (int)p.stride[k];
 }
 
-// Spin until *f >= e.  Returns false on timeout / abort (watchdog).
 // This launch's epoch (a6), read once per CTA from the comm's device counter
 // (so a collective captured in a CUDA graph gets a fresh epoch on every replay).
 __shared__ uint32_t s_epoch;
 __device__ __forceinline__ uint32_t cur_epoch() { return s_epoch; }
 
+// Spin until *f >= e.  Returns false on timeout / abort (watchdog).
 __device__ bool wait_geq(const KParams& p, const uint32_t* f, uint32_t e, uint32_t where) {
   if (dev::ld_acquire_sys(f) >= e) return true;
   const uint64_t t0 = dev::globaltimer();
@@ -297,12 +297,10 @@ template <class Tag>
 __device__ void run_op_ldg(const KParams& p, const OpDesc& d, int gi, int gn) {
   const int k = d.dim, pk = p.size[k];
   const int mode = unit_mode(d);
-  const uint64_t Lv = p.slice_elems * p.elem_size / 16;
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
     const Item m = decode_item(p, d, mode, 0, it);
     uint4* dst = reinterpret_cast<uint4*>(data_of(p, m.q) + m.off);
     const PeerSrc src{&p, m.g0, (int)p.stride[k], m.off};
-    (void)Lv;
     if (mode == U_DIRECT_AG) {
       dev::copy_range<8>(dst, src(m.j), a / 16, e / 16);
       return;
