@@ -141,7 +141,7 @@ def nvlink_bytes_per_rank(plan, cross):
 def run_themis(a):
     import torch
     from paper_2110_04478_b200 import themis as th
-    from paper_2110_04478_b200.dist import barrier, init_from_env, max_over_ranks
+    from paper_2110_04478_b200.dist import barrier, check_same_plan, init_from_env, max_over_ranks
     from synth import device_input
 
     os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (NCCL prints its version at INFO)
@@ -193,6 +193,7 @@ def run_themis(a):
         t = th.Topology(SIZES, bw)
         p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO,
                     concurrency=a.concurrency)
+        check_same_plan(p, group)            # fail fast before any kernel (R22)
         p.bind(comm, th.default_ctas(rat, total_ctas))
         return p
 
@@ -364,6 +365,7 @@ def run_themis(a):
             release_ns = 0
             hplan = th.Plan(th.Topology(SIZES, ratio), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
                             concurrency=a.concurrency)
+        check_same_plan(hplan, group)
         hplan.bind(comm, th.default_ctas(ratio, total_ctas))
         th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "f32", hplan)
         torch.cuda.synchronize()

@@ -57,3 +57,17 @@ def barrier(group=None, device=None) -> None:
             dist.barrier(group=group, device_ids=[device.index])
         else:
             dist.barrier(group=group)
+
+
+def check_same_plan(plan, group=None) -> None:
+    """Fail fast on the host if the ranks built different plans (the kernel's
+    entry check would latch THEMIS_ERR_PLAN_MISMATCH, R22): all-gathers the
+    plan hash (inputs, schedule, per-dim order) and raises ValueError naming
+    the ranks that differ from rank 0.  No-op without a process group."""
+    import torch.distributed as dist
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return
+    hashes = allgather_bytes(int(plan.info["hash"]).to_bytes(8, "little"), group)
+    bad = [r for r, h in enumerate(hashes) if h != hashes[0]]
+    if bad:
+        raise ValueError(f"ranks {bad} built a different plan than rank 0 (plan hash differs)")

@@ -47,6 +47,46 @@ def test_gloo_handle_exchange_and_max():
         assert firsts == [0, 1] and n == 64 and m == 2.5
 
 
+def _plan_worker(rank, world, port, q, same):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    from paper_2110_04478_b200 import themis as th
+    from paper_2110_04478_b200.dist import check_same_plan, init_from_env
+    r, w, local, group = init_from_env("gloo")
+    try:
+        # e.g. a per-rank measured H2D rate leaking into chunk_release_ns
+        release = 1000 if same else 1000 + r
+        plan = th.Plan(th.Topology((2, 2), (100000, 50000)), th.ALLREDUCE, 1 << 24, 16, chunk_release_ns=release)
+        try:
+            check_same_plan(plan, group)
+            q.put((r, "ok"))
+        except ValueError as e:
+            q.put((r, str(e)))
+        plan.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_plan_consistency_check():
+    """Plans must be identical on every rank (R22); the host-side check
+    catches a rank-dependent input before any kernel runs."""
+    for same in (True, False):
+        port = _free_port()
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        ps = [ctx.Process(target=_plan_worker, args=(r, 2, port, q, same)) for r in range(2)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(120)
+            assert p.exitcode == 0
+        res = dict(q.get() for _ in range(2))
+        if same:
+            assert res == {0: "ok", 1: "ok"}
+        else:
+            assert all("ranks [1]" in v for v in res.values())
+
+
 def test_rank_layout_helpers():
     from bench import logical_layout
     lay = logical_layout((2, 2, 2), 4)
