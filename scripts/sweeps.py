@@ -36,6 +36,7 @@ from synth import WORKLOAD_PARAMS, bucket_sizes, device_input, torch_dtype  # no
 import bench  # noqa: E402
 
 CONC = 1
+LAT = 0       # --latency-ns: measured per-op A_K for the latency-aware auto-chunk column (config 3)
 
 
 class Runner:
@@ -120,6 +121,21 @@ def config3(r: Runner, quick):
                             plan.close()
                         row[f"{mode}_speedup"] = round(row[f"{mode}_themis_bus_gbs"] / row[f"{mode}_baseline_bus_gbs"],
                                                        3)
+                        if LAT and mode == "paced" and C == 64:   # once per (size, ratio)
+                            # latency-aware Themis with the planner-chosen chunk count (R25, NEXT-1)
+                            t = th.Topology(tuple(sizes), tuple(bw), None, tuple([LAT] * len(sizes)))
+                            try:
+                                plan = th.Plan(t, th.ALLREDUCE, S, th.AUTO_CHUNKS, th.THEMIS, th.SCF,
+                                               charge_latency=True)
+                                plan.bind(comm, th.default_ctas(rat, r.ctas_total))
+                                sec = r.time(comm, plan, th.ALLREDUCE, S // 4, "f32")
+                                row["paced_themis_auto_bus_gbs"] = round(2 * S * (P - 1) / P / sec / 1e9, 2)
+                                row["paced_themis_auto_chunks"] = plan.n_chunks
+                                row["paced_auto_vs_baseline"] = round(row["paced_themis_auto_bus_gbs"] /
+                                                                      row["paced_baseline_bus_gbs"], 3)
+                                plan.close()
+                            except th.ThemisError as e:
+                                row["paced_themis_auto_error"] = str(e)
                     comm.set_pacing(False)
                     r.emit(row)
         comm.close()
@@ -193,12 +209,15 @@ def main():
     ap.add_argument("--config", type=int, required=True, choices=[3, 4, 5])
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--concurrency", type=int, default=1, help="ops in flight per dim (plans)")
+    ap.add_argument("--latency-ns", type=int, default=0,
+                    help="config 3: also time a latency-aware Themis plan with planner-chosen chunks (A_K ns)")
     a = ap.parse_args()
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     torch.cuda.set_device(local)
-    global CONC
+    global CONC, LAT
     CONC = a.concurrency
+    LAT = a.latency_ns
     r = Runner(group, rank, world, local)
     {3: config3, 4: config4, 5: config5}[a.config](r, a.quick)
     if world > 1:
