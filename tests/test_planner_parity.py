@@ -291,3 +291,26 @@ def test_max_dims_and_chunks():
         th.Plan(th.Topology((2,) * 9, (1,) * 9), th.ALLREDUCE, 1 << 20, 4)
     with pytest.raises(th.ThemisError):
         th.Plan(th.Topology((2, 2), (1, 1)), th.ALLREDUCE, 1 << 20, 1025)
+
+
+def test_random_small_configs_10k():
+    """SURVEY.md §4 tier 3: >= 10^4 random (topology, bytes, C, policy, intra)
+    tuples, small enough to run in well under a minute, every field bit-exact."""
+    rng = random.Random(2110_04478)
+    skipped = 0
+    for _ in range(10_000):
+        D = rng.randint(1, 3)
+        sizes = [rng.choice([2, 3, 4, 8]) for _ in range(D)]
+        bw = [rng.choice([1, 2, 3, 4, 5, 7, 8, 16]) * rng.choice([1, 1000, 50000]) for _ in range(D)]
+        lat = [rng.choice([0, 0, rng.randint(1, 5000)]) for _ in range(D)]
+        o, g = make_pair(sizes, bw, None, lat)
+        coll = rng.choice([S.AR, S.AR, "RS", "AG"])
+        nbytes = rng.randint(1, 1 << 16) * rng.choice([1, 16, 4096])
+        try:
+            compare(o, g, coll, nbytes, rng.randint(1, 8), rng.choice([S.BASELINE, S.THEMIS]),
+                    rng.choice([E.SCF, E.FIFO, E.SCF_LITERAL]), 16, rng.random() < 0.3,
+                    release=rng.choice([0, 0, 0, rng.randint(1, 100_000)]))
+        except th.ThemisError as e:
+            assert e.status == 4
+            skipped += 1
+    assert skipped < 200
