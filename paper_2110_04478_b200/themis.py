@@ -148,6 +148,19 @@ class Plan:
         check(lib().themis_plan_times(self.h, s.ctypes.data, e.ctypes.data))
         return s, e
 
+    def to_csv(self) -> str:
+        """Schedule export: `chunk_id,rs_order,ag_order,bytes`,
+        1-based dims, bytes = S / C — the format the oracle writes, so a plan
+        can be saved, diffed and replayed (themis_plan_custom)."""
+        rs, ag = self.orders()
+        cb = Fraction(self.nbytes, self.n_chunks)
+        lines = ["chunk_id,rs_order,ag_order,bytes"]
+        for c in range(self.n_chunks):
+            r = " ".join(str(int(d) + 1) for d in rs[c] if d != 0xFF)
+            a = " ".join(str(int(d) + 1) for d in ag[c] if d != 0xFF)
+            lines.append(f"{c},{r},{a},{cb}")
+        return "\n".join(lines) + "\n"
+
     def makespan_ns(self) -> Fraction:
         return Fraction(self.info["makespan"], self.info["time_scale"])
 

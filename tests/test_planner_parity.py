@@ -314,3 +314,16 @@ def test_random_small_configs_10k():
             assert e.status == 4
             skipped += 1
     assert skipped < 200
+
+
+@pytest.mark.parametrize("coll", [S.AR, "RS", "AG"])
+def test_csv_export_matches_oracle(coll):
+    """Plan export is byte-identical to the oracle's export."""
+    o, g = make_pair((2, 4, 2), (300000, 200000, 100000))
+    for nbytes, C in ((1 << 24, 16), (1000, 3)):
+        sched = S.schedule_collective(o, coll, nbytes, C, S.THEMIS)
+        plan = th.Plan(g, COLLS[coll], nbytes, C, th.THEMIS)
+        try:
+            assert plan.to_csv() == S.export_csv(sched)
+        finally:
+            plan.close()
