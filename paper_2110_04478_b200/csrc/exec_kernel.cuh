@@ -191,23 +191,28 @@ __device__ __forceinline__ uint64_t part_stride(const KParams& p, int k) {
 // the jj-th peer (jj = 0..P_k-2) of a rank with coordinate ck on its dim
 __device__ __forceinline__ int peer_member(int jj, int ck) { return jj < ck ? jj : jj + 1; }
 
-__device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, int mode, int step, uint64_t it) {
+// 32-bit index arithmetic throughout: a unit has < 2^32 items (V * nblk *
+// (P_k - 1) <= 64^3), and 64-bit div/mod (emulated, ~100 instructions each)
+// made small ops latency-bound on this decode.
+__device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, int mode, int step, uint64_t it64) {
   Item r;
   const int k = d.dim, pk = p.size[k];
-  int64_t f;
+  const uint32_t it = (uint32_t)it64, nblk = (uint32_t)d.nblk;
+  uint32_t f;
   int digit;
   if (mode == U_DIRECT_AG) {
-    const uint64_t per_v = (uint64_t)(pk - 1) * d.nblk;
-    r.q = p.my_gpu * p.V + (int)(it / per_v);
-    const uint64_t rem = it % per_v;
-    const int jj = (int)(rem / d.nblk);
+    const uint32_t per_v = (uint32_t)(pk - 1) * nblk;
+    const uint32_t vq = it / per_v, rem = it - vq * per_v;
+    r.q = p.my_gpu * p.V + (int)vq;
+    const uint32_t jj = rem / nblk;
     const int ck = coord(p, r.q, k);
-    r.j = jj < ck ? jj : jj + 1;
-    f = (int64_t)(rem % d.nblk);
+    r.j = (int)jj < ck ? (int)jj : (int)jj + 1;
+    f = rem - jj * nblk;
     digit = r.j;
   } else {
-    r.q = p.my_gpu * p.V + (int)(it / d.nblk);
-    f = (int64_t)(it % d.nblk);
+    const uint32_t vq = it / nblk;
+    r.q = p.my_gpu * p.V + (int)vq;
+    f = it - vq * nblk;
     r.j = -1;
     const int ck = coord(p, r.q, k);
     digit = mode == U_DIRECT_RS   ? ck
@@ -215,12 +220,13 @@ __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, i
           : mode == U_RING_RS     ? (ck + pk - 2 - step) % pk
                                   : ((ck - 1 - step) % pk + pk) % pk;
   }
-  int64_t b = (int64_t)digit * p.stride[k];
+  int b = digit * (int)p.stride[k];
   for (int dd = 0; dd < p.D; ++dd)  // other fixed digits: the rank's coords on the reduced dims
-    if ((d.reduced >> dd & 1u) && dd != k) b += (int64_t)coord(p, r.q, dd) * p.stride[dd];
+    if ((d.reduced >> dd & 1u) && dd != k) b += coord(p, r.q, dd) * (int)p.stride[dd];
   for (int i = 0; i < d.nfree; ++i) {
-    b += (f % d.free_size[i]) * d.free_stride[i];
-    f /= d.free_size[i];
+    const uint32_t fs = (uint32_t)d.free_size[i], fq = f / fs;
+    b += (int)(f - fq * fs) * (int)d.free_stride[i];
+    f = fq;
   }
   r.g0 = r.q - coord(p, r.q, k) * (int)p.stride[k];
   r.off = ((uint64_t)b * p.blk_elems + (uint64_t)d.chunk * p.slice_elems) * p.elem_size;

@@ -15,6 +15,7 @@ from paper_2110_04478_b200.dist import init_from_env  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="2,2,2")
 ap.add_argument("--mib", type=int, default=16)
+ap.add_argument("--kib", type=int, default=0, help="size in KiB (overrides --mib)")
 ap.add_argument("--chunks", type=int, default=64)
 ap.add_argument("--ctas", default="8,8,8")
 ap.add_argument("--policy", default="baseline")
@@ -24,7 +25,7 @@ rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SI
 torch.cuda.set_device(local)
 sizes = tuple(int(x) for x in a.sizes.split(","))
 topo = th.Topology(sizes, (1,) * len(sizes))
-N = (a.mib << 20) // 4
+N = ((a.kib << 10) if a.kib else (a.mib << 20)) // 4
 comm = th.Comm(topo, N * 4, group=group, device=local)
 comm.set_stages(4)
 comm.enable_trace(2)
@@ -55,6 +56,9 @@ if rank == 0:
     print(f"  {'published':20s} median {np.median(rel(tr[:, :, 1])):7.2f} us")
     lat = [tr[c, s, 0] - tr[c, s - 1, 1] for c in range(tr.shape[0]) for s in range(1, tr.shape[1])]
     print(f"  stage transition median {np.median(lat)/1e3:.2f} us p10 {np.percentile(lat, 10)/1e3:.2f}")
+    for c, s_ in ((1, 1), (2, 3), (3, 4)):                    # a few raw ops, relative to the op start
+        print(f"  op (c{c}, s{s_}) rel us:", [round((x - st[c, s_]) / 1e3, 2) for x in de[c, s_, :6]],
+              "end", round((tr[c, s_, 1] - st[c, s_]) / 1e3, 2))
     # per (dim, phase): median op duration and the per-rank bytes it moves -> GB/s
     rs, ag = plan.orders()
     D = len(sizes)
