@@ -194,8 +194,13 @@ def run_themis(a):
         p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO,
                     concurrency=a.concurrency)
         check_same_plan(p, group)            # fail fast before any kernel (R22)
-        p.bind(comm, th.default_ctas(rat, total_ctas))
+        p.bind(comm, caps_for(rat))
         return p
+
+    def caps_for(rat):
+        if a.ctas_split and tuple(rat) == tuple(ratio):
+            return [int(x) for x in a.ctas_split.split(",")]
+        return th.default_ctas(rat, total_ctas)
 
     def timed(plan, steps, warmup):
         for _ in range(warmup):
@@ -366,7 +371,7 @@ def run_themis(a):
             hplan = th.Plan(th.Topology(SIZES, ratio), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
                             concurrency=a.concurrency)
         check_same_plan(hplan, group)
-        hplan.bind(comm, th.default_ctas(ratio, total_ctas))
+        hplan.bind(comm, caps_for(ratio))
         th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, N, "f32", hplan)
         torch.cuda.synchronize()
         k = max(1, min(a.steps, 3))
@@ -532,6 +537,7 @@ def main():
     ap.add_argument("--chunks", type=int, default=64)
     ap.add_argument("--ratio", default="4:2:1", help="emulated BW(dim1):BW(dim2):BW(dim3)")
     ap.add_argument("--ctas-total", type=int, default=0, help="CTAs split over the dims (default: all SMs)")
+    ap.add_argument("--ctas-split", default="", help="explicit CTAs per dim for the headline ratio (experiments)")
     ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")
     ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
     ap.add_argument("--no-compare", action="store_true")
