@@ -306,18 +306,7 @@ class Comm:
         return out.reshape(plan.info["n_chunks"], plan.info["n_stages"], 2)
 
     # -- convenience: tensors in, tensors out (copies through the heap) -------
-    def all_reduce(self, tensors, n_chunks: int = 64, policy: int = THEMIS, bw_mbps=None,
-                   ctas_per_dim: Optional[Sequence[int]] = None, stream=None):
-        """All-Reduce user tensors in place: one tensor (V = 1) or a list of V
-        tensors, one per local logical rank, same numel / dtype.
-
-        Any numel (R17): the copy into the heap is zero-padded up to the
-        executor's granule P·C·(16 B / elem), the collective runs on the
-        padded buffer (zeros add nothing) and the first numel elements are
-        copied back.  Plans are cached per (bytes, chunks, policy, bw, CTAs)
-        (PAPER.md:532).  The copies are extra HBM traffic: latency-critical
-        callers write into `rank_view` and call `themis_allreduce` directly.
-        """
+    def _tensors(self, tensors):
         import torch
         ts = [tensors] if isinstance(tensors, torch.Tensor) else list(tensors)
         if len(ts) != self.V:
@@ -328,22 +317,44 @@ class Comm:
         n = ts[0].numel()
         if any(t.numel() != n or t.dtype != ts[0].dtype or t.device != self.device for t in ts):
             raise ValueError("tensors must share numel, dtype and this comm's device")
-        if n == 0:                                   # nothing to reduce (every rank must agree: same numel)
-            return tensors
-        g = self.P * (n_chunks or AUTO_MAX_CHUNKS) * (16 // ELEM_SIZE[dt])   # 0 = auto: every candidate fits
-        count = max(g, (n + g - 1) // g * g)
-        nbytes = count * ELEM_SIZE[dt]
+        return ts, dt, n
+
+    def _plan(self, coll, nbytes, n_chunks, policy, bw_mbps, ctas_per_dim) -> "Plan":
+        """Plans cached per (collective, bytes, chunks, policy, bw, CTAs)."""
         if nbytes > self.vrank_stride:
-            raise ValueError(f"{nbytes} B padded exceeds the heap's {self.vrank_stride} B per rank")
+            raise ValueError(f"{nbytes} B exceeds the heap's {self.vrank_stride} B per rank")
         bw = tuple(bw_mbps or self.topo.bw_mbps)
-        key = (nbytes, n_chunks, policy, bw, None if ctas_per_dim is None else tuple(ctas_per_dim))
+        key = (coll, nbytes, n_chunks, policy, bw, None if ctas_per_dim is None else tuple(ctas_per_dim))
         cache = self.__dict__.setdefault("_plans", {})
         plan = cache.get(key)
         if plan is None:
             topo = Topology(self.topo.sizes, bw, self.topo.kinds, self.topo.latency_ns)
-            plan = Plan(topo, ALLREDUCE, nbytes, n_chunks, policy, SCF if policy == THEMIS else FIFO)
+            plan = Plan(topo, coll, nbytes, n_chunks, policy, SCF if policy == THEMIS else FIFO)
             plan.bind(self, ctas_per_dim)
             cache[key] = plan
+        return plan
+
+    def _granule(self, n_chunks, dt):
+        return self.P * (n_chunks or AUTO_MAX_CHUNKS) * (16 // ELEM_SIZE[dt])
+
+    def all_reduce(self, tensors, n_chunks: int = 64, policy: int = THEMIS, bw_mbps=None,
+                   ctas_per_dim: Optional[Sequence[int]] = None, stream=None):
+        """All-Reduce user tensors in place: one tensor (V = 1) or a list of V
+        tensors, one per local logical rank, same numel / dtype.
+
+        Any numel (R17): the copy into the heap is zero-padded up to the
+        executor's granule P·C·(16 B / elem), the collective runs on the
+        padded buffer (zeros add nothing) and the first numel elements are
+        copied back.  The copies are extra HBM traffic: latency-critical
+        callers write into `rank_view` and call `themis_allreduce` directly.
+        """
+        import torch
+        ts, dt, n = self._tensors(tensors)
+        if n == 0:                                   # nothing to reduce (every rank must agree: same numel)
+            return tensors
+        g = self._granule(n_chunks, dt)             # 0 = auto: every candidate fits
+        count = max(g, (n + g - 1) // g * g)
+        plan = self._plan(ALLREDUCE, count * ELEM_SIZE[dt], n_chunks, policy, bw_mbps, ctas_per_dim)
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         with torch.cuda.stream(s):
             for v, t in enumerate(ts):
@@ -355,6 +366,48 @@ class Comm:
             for v, t in enumerate(ts):
                 t.copy_(self.rank_view(v, n, dt).view(t.shape))
         return tensors
+
+    def reduce_scatter(self, tensors, n_chunks: int = 64, policy: int = THEMIS, bw_mbps=None,
+                       ctas_per_dim: Optional[Sequence[int]] = None, stream=None) -> list:
+        """Reduce-Scatter: V full-size inputs (numel a multiple of P·C·16 B /
+        elem); returns, per local rank q, a new tensor holding block q of the
+        sum (output block r at r·numel/P, R16)."""
+        import torch
+        ts, dt, n = self._tensors(tensors)
+        if n % self._granule(n_chunks, dt):
+            raise ThemisError(2, f"numel must be a multiple of {self._granule(n_chunks, dt)}")
+        plan = self._plan(REDUCE_SCATTER, n * ELEM_SIZE[dt], n_chunks, policy, bw_mbps, ctas_per_dim)
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        blk = n // self.P
+        with torch.cuda.stream(s):
+            for v, t in enumerate(ts):
+                self.rank_view(v, n, dt).copy_(t.reshape(-1))
+            themis_reduce_scatter(self.data_ptr, n, dt, plan, s)
+            out = []
+            for v in range(self.V):
+                q = self.gpu_rank * self.V + v
+                out.append(self.rank_view(v, n, dt)[q * blk:(q + 1) * blk].clone())
+        return out
+
+    def all_gather(self, blocks, n_chunks: int = 64, policy: int = THEMIS, bw_mbps=None,
+                   ctas_per_dim: Optional[Sequence[int]] = None, stream=None) -> list:
+        """All-Gather: V per-rank blocks (numel m, m·P a multiple of P·C·16 B /
+        elem); returns, per local rank, a new tensor of all P blocks in rank
+        order."""
+        import torch
+        ts, dt, m = self._tensors(blocks)
+        n = m * self.P
+        if n % self._granule(n_chunks, dt):
+            raise ThemisError(2, f"numel * P must be a multiple of {self._granule(n_chunks, dt)}")
+        plan = self._plan(ALL_GATHER, n * ELEM_SIZE[dt], n_chunks, policy, bw_mbps, ctas_per_dim)
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        with torch.cuda.stream(s):
+            for v, t in enumerate(ts):
+                q = self.gpu_rank * self.V + v
+                self.rank_view(v, n, dt)[q * m:(q + 1) * m].copy_(t.reshape(-1))
+            themis_all_gather(self.data_ptr, n, dt, plan, s)
+            out = [self.rank_view(v, n, dt).clone() for v in range(self.V)]
+        return out
 
     def close(self):
         for p in self.__dict__.pop("_plans", {}).values():

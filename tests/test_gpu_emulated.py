@@ -478,3 +478,28 @@ def test_tensor_all_reduce_empty():
         assert all(t.numel() == 0 for t in ts)
     finally:
         comm.close()
+
+
+def test_tensor_reduce_scatter_all_gather():
+    """Comm.reduce_scatter / all_gather on user tensors: RS block r == block r
+    of the sum, AG == the concatenation of all blocks, int32 exact; the
+    granule is enforced."""
+    topo = th.Topology((2, 4), (2, 1))
+    P, C_ = 8, 4
+    n = P * C_ * 4 * 33
+    comm = th.Comm(topo, n * 4)
+    try:
+        xs = host_inputs(P, n, "i32")
+        outs = comm.reduce_scatter([torch.from_numpy(x).cuda() for x in xs], n_chunks=C_)
+        want = O.allreduce_definition(xs, "i32")
+        blk = n // P
+        for r in range(P):
+            assert np.array_equal(outs[r].cpu().numpy(), want[r * blk:(r + 1) * blk])
+        gathered = comm.all_gather(outs, n_chunks=C_)
+        for r in range(P):
+            assert np.array_equal(gathered[r].cpu().numpy(), want)
+        with pytest.raises(th.ThemisError):
+            comm.reduce_scatter([torch.zeros(n + 4, dtype=torch.int32, device="cuda")] * P, n_chunks=C_)
+        comm.status()
+    finally:
+        comm.close()
