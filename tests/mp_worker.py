@@ -153,6 +153,70 @@ def nccl_and_stress_case(group, W, g, iters=60):
     return bad
 
 
+def api_case(group, W, g):
+    """User-facing paths at W GPUs: Comm.all_reduce on ragged tensors,
+    Comm.reduce_scatter / all_gather, themis_allreduce_host (chunk-streamed,
+    with a chunk-arrival plan) and a CUDA-graph replay — int32 exact against
+    the plain definitions.  Returns the number of mismatches on this GPU."""
+    topo = th.Topology((2, 2, 2), (1, 1, 1))
+    P = 8
+    V = P // W
+    bad = 0
+    comm = th.Comm(topo, 1 << 22, group=group)
+    comm.set_timeout(20.0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    # ragged all_reduce
+    n = 12345
+    xs = host_inputs(P, n, "i32", seed=7)
+    ts = [torch.from_numpy(xs[g * V + v]).to(dev) for v in range(V)]
+    comm.all_reduce(ts, n_chunks=4)
+    want = O.allreduce_definition(xs, "i32")
+    bad += sum(not np.array_equal(t.cpu().numpy(), want) for t in ts)
+    # reduce_scatter -> all_gather
+    n = P * 4 * 4 * 16
+    xs = host_inputs(P, n, "i32", seed=8)
+    outs = comm.reduce_scatter([torch.from_numpy(xs[g * V + v]).to(dev) for v in range(V)], n_chunks=4)
+    want = O.allreduce_definition(xs, "i32")
+    blk = n // P
+    bad += sum(not np.array_equal(outs[v].cpu().numpy(), want[(g * V + v) * blk:(g * V + v + 1) * blk])
+               for v in range(V))
+    full = comm.all_gather(outs, n_chunks=4)
+    bad += sum(not np.array_equal(f.cpu().numpy(), want) for f in full)
+    # host buffers, chunk-streamed with an arrival-time plan
+    n = P * 16 * 4 * 8
+    xs = host_inputs(P, n, "i32", seed=9)
+    plan = th.Plan(th.Topology((2, 2, 2), (4000, 2000, 1000)), th.ALLREDUCE, n * 4, 16,
+                   chunk_release_ns=5000).bind(comm)
+    hin = torch.from_numpy(np.concatenate([xs[g * V + v] for v in range(V)])).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    for _ in range(2):
+        th.themis_allreduce_host(hin.data_ptr(), hout.data_ptr(), comm.data_ptr, n, "i32", plan)
+    torch.cuda.synchronize()
+    want = O.allreduce_definition(xs, "i32")
+    bad += sum(not np.array_equal(hout.numpy()[v * n:(v + 1) * n], want) for v in range(V))
+    # CUDA graph: two All-Reduces captured, replayed twice
+    for v in range(V):
+        comm.rank_view(v, n, "i32").copy_(torch.from_numpy(xs[g * V + v]))
+    torch.cuda.synchronize()
+    gph, st = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(gph, stream=st):
+            th.run(th.ALLREDUCE, comm, plan, n, "i32")
+            th.run(th.ALLREDUCE, comm, plan, n, "i32")
+    torch.cuda.synchronize()
+    for _ in range(2):
+        gph.replay()
+    torch.cuda.synchronize()
+    w = xs
+    for _ in range(4):
+        w = [O.allreduce_definition(w, "i32")] * P
+    bad += sum(not np.array_equal(comm.rank_view(v, n, "i32").cpu().numpy(), w[0]) for v in range(V))
+    comm.status()
+    plan.close()
+    comm.close()
+    return bad
+
+
 def fault_case(group, W, g):
     """Fault injection: rank 1 launches a plan
     with a different intra-dimension policy.  Every rank must report
@@ -199,6 +263,10 @@ def main():
         if bad:
             fails.append((c, bad))
     import torch.distributed as dist
+    if 8 % W == 0:
+        nb = api_case(group, W, rank)
+        if nb:
+            fails.append((("tensor API / host streaming / CUDA graph",), [f"{nb} mismatches"]))
     st = fault_case(group, W, rank)
     if st != 6:
         fails.append((("fault-injection plan mismatch",), [f"status {st}"]))
