@@ -27,7 +27,7 @@ sizes = tuple(int(x) for x in a.sizes.split(","))
 topo = th.Topology(sizes, (1,) * len(sizes))
 N = ((a.kib << 10) if a.kib else (a.mib << 20)) // 4
 comm = th.Comm(topo, N * 4, group=group, device=local)
-comm.set_stages(4)
+comm.set_stages(int(os.environ.get("PROBE_STAGES", "4")))
 comm.enable_trace(2)
 for v in range(comm.V):
     comm.rank_view(v, N, "f32").fill_(1.0)
