@@ -429,7 +429,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
           uint4* dj = reinterpret_cast<uint4*>(base + pos + (uint64_t)peer_member(j, ck) * ps);
           for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dj + w, sm[w]);
           __syncwarp();
-          if (lane == 0) dev::mbar_arrive(&empty[s]);
+          if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);  // slot reads done; stores ordered by op_done
         }
       }
       return;
@@ -461,7 +461,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
       }
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
+      if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);  // slot reads done; stores ordered by op_done
     }
   });
   return ok;
