@@ -168,17 +168,21 @@ def run_themis(a):
         total_ctas = min(sms, 32 * len(SIZES) + 32) if len(SIZES) > 1 else 32
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
-    # ring depth: 6 when some dims are GPU-local (profiles/r01/stages/: N = 2 / 4
-    # gain 2-4 % over 4); all-NVLink topologies peak lower (calibration above)
+    # TMA ring (stages x stage bytes, <= 192 KiB): larger tiles cut the fixed
+    # per-tile cost (profiles/r01/stagekb/: 3 x 64 KiB +0.8 % at N = 1, 4 x 48
+    # KiB +2 % at N = 4 over 6 x 32); all-NVLink topologies want fewer bytes in
+    # flight per GPU (calibration above: 3 x 32 KiB)
     if ncross_ == len(SIZES):
-        stages = a.stages or (3 if len(SIZES) > 1 else 4)
+        stages, stage_kb = a.stages or (3 if len(SIZES) > 1 else 4), a.stage_kb or 32
+    elif ncross_ == 0:
+        stages, stage_kb = a.stages or 3, a.stage_kb or 64
     else:
-        stages = a.stages or 6
+        stages, stage_kb = a.stages or 4, a.stage_kb or 48
     topo = th.Topology(SIZES, ratio)
     comm = th.Comm(topo, S, group=group, device=local)
     comm.set_timeout(30.0)
     comm.set_stages(1)
-    comm.set_stage_bytes(a.stage_kb * 1024)
+    comm.set_stage_bytes(stage_kb * 1024)
     comm.set_stages(stages)
     pristine = [device_input(rank * V + v, N, "f32", dev) for v in range(V)]
 
@@ -440,7 +444,7 @@ def run_themis(a):
                        "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
                        "ops_in_flight_per_dim": max(1, a.concurrency),
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
-                       "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages,
+                       "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages, "tma_stage_kib": stage_kb,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
                        "aggregate_bus_gbs": round(busbw(t_main) * P, 1),
                        "best_step_bus_gbs": round(busbw(t_best), 2),
@@ -544,7 +548,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
-    ap.add_argument("--stage-kb", type=int, default=32, help="TMA ring stage size (KiB)")
+    ap.add_argument("--stage-kb", type=int, default=0, help="TMA ring stage size (KiB; default by topology)")
     ap.add_argument("--concurrency", type=int, default=1,
                     help="ops in flight per dimension in the plan's pre-simulation (1 = the paper's model)")
     ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")
