@@ -58,6 +58,18 @@ def _np_dtype(dtype: str):
             "i32": np.int32, "f64": np.float64}[dtype]
 
 
+def reduce_hops(parts, dtype: str) -> np.ndarray:
+    """Ring dims (R18 amended): the partial travels the ring as a message in
+    the buffer's dtype, so it is rounded after every hop:
+    acc = parts[0]; acc = round(acc + parts[j]) for j = 1.. (fp32 adds)."""
+    if dtype in ("f32", "i32", "f64"):
+        return reduce_in_order(parts, dtype)       # storing the partial rounds nothing
+    acc = parts[0]
+    for p in parts[1:]:
+        acc = reduce_in_order([acc, p], dtype)
+    return acc
+
+
 def reduce_in_order(parts, dtype: str) -> np.ndarray:
     """sum_j parts[j] in coordinate order j with the dtype's arithmetic."""
     if dtype == "f32":
@@ -110,6 +122,11 @@ def _groups(topo, k):
     return [topo.dim_peers(r, k) for r in range(topo.P) if topo.coords(r)[k] == 0]
 
 
+def ring_hops(topo, k) -> bool:
+    """Table 1 ring dims with P_k >= 3 run the ring algorithm (P_k = 2 is direct)."""
+    return topo.dims[k].kind == "ring" and topo.dims[k].size >= 3
+
+
 def summation_order(topo, k, t) -> list:
     """Member order in which part t (digit_k = t) is summed on dim k.
     Direct / switch dims: coordinate order 0..P_k-1 (R18).  Ring dims
@@ -132,7 +149,8 @@ def apply_rs(bufs, topo, C, c, k, reduced, dtype):
                 if digit(topo, b, k) != t:
                     continue
                 s = slice_of(N, topo.P, C, c, b)
-                new.append((mt, s, reduce_in_order([bufs[members[j]][s] for j in order], dtype)))
+                red = reduce_hops if ring_hops(topo, k) else reduce_in_order
+                new.append((mt, s, red([bufs[members[j]][s] for j in order], dtype)))
         for mt, s, v in new:
             bufs[mt][s] = v
 
@@ -198,7 +216,8 @@ def allreduce_element(vals, topo, rs_order, dtype: str, block: int):
     stage structure: arrange the P ranks' values of the element on the
     P_1 x ... x P_D grid and reduce along the chunk's RS dims in `rs_order`,
     each axis in the dim's summation order (coordinate order; ring dims end at
-    the owner digit of `block`), with the dtype's rounding per stage (R18).
+    the owner digit of `block`), with the dtype's rounding per stage (per hop
+    on ring dims, R18).
     AG only copies, so every rank ends with this value.  `vals[r]` is rank r's
     value (bf16 as uint16 bits).  Used to check full-size runs on samples."""
     P = topo.P
@@ -220,7 +239,7 @@ def allreduce_element(vals, topo, rs_order, dtype: str, block: int):
                 members.append(live[tuple(cc)])
             out = list(coords)
             out[k] = t
-            nxt[tuple(out)] = reduce_in_order(members, dtype)
+            nxt[tuple(out)] = (reduce_hops if ring_hops(topo, k) else reduce_in_order)(members, dtype)
         # keep only the owner digit along k (the other digits are not held)
         live = {}
         for coords, v in nxt.items():

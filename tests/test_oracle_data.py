@@ -213,6 +213,32 @@ def _ring_rs_message_passing(parts, dtype_add):
     return [dtype_add(partial[(t, t)], parts[t][t]) for t in range(P)]
 
 
+def test_ring_low_precision_messages_match_message_passing():
+    """bf16 / f16 ring dims (R18 amended): every hop's message is a partial in
+    the buffer's dtype, so the partial is rounded at every hop — the oracle
+    matches an explicit message-passing ring whose messages are bf16 / f16
+    values, bit for bit, and differs from a single final rounding."""
+    for dtype in ("bf16", "f16"):
+        if dtype == "bf16":
+            add = lambda a, b: O.f32_to_bf16(O.bf16_to_f32(a) + O.bf16_to_f32(b))  # noqa: E731
+        else:
+            add = lambda a, b: (a.astype(np.float32) + b.astype(np.float32)).astype(np.float16)  # noqa: E731
+        differs = False
+        for P in (3, 4, 5):
+            t = T.Topology.make((P,), (1,), (T.RING,))
+            N = P * 64
+            x = host_inputs(P, N, dtype, seed=91 + P, dist="wide")
+            out = O.run_schedule(x, _sched(t, "RS", N, 4, 1, [(0,)]), dtype)
+            blk = N // P
+            parts = [[x[m][q * blk:(q + 1) * blk] for q in range(P)] for m in range(P)]
+            want = _ring_rs_message_passing(parts, add)
+            for r in range(P):
+                assert np.array_equal(out[r][r * blk:(r + 1) * blk].view(np.uint16), want[r].view(np.uint16))
+                once = O.reduce_in_order([parts[(r + 1 + i) % P][r] for i in range(P)], dtype)
+                differs |= not np.array_equal(once.view(np.uint16), want[r].view(np.uint16))
+        assert differs     # the per-hop rounding is observable on these inputs
+
+
 def test_ring_summation_order_matches_message_passing():
     """The oracle's ring RS (closed-form member order) equals an explicit
     message-passing ring on floats, bit for bit (order matters for floats)."""
