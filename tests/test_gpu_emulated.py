@@ -89,8 +89,11 @@ def check_ar(sizes, bw, dtype, C, slice_elems, policy=th.THEMIS, **kw):
     scale = O.abs_sum(xs, dtype)
     # north_star tolerance on the recipe inputs; on the adversarial "wide"
     # inputs the F10 worst-case bound (one RNE per RS stage: D * 2^-8 for bf16)
-    # (F10: one RNE per RS stage -> D * 2^-8 for bf16, D * 2^-11 for f16)
-    wide = {"bf16": len(sizes) * 2.0 ** -8, "f16": len(sizes) * 2.0 ** -11, "f32": TOL["f32"]}
+    # (F10: one RNE per RS stage -> D * 2^-8 for bf16, D * 2^-11 for f16; a ring
+    # dim of P_k >= 3 rounds at each of its P_k - 1 hops, R18)
+    kinds_ = kw.get("kinds") or (th.DIRECT,) * len(sizes)
+    rounds = sum(pk - 1 if kd == th.RING and pk >= 3 else 1 for pk, kd in zip(sizes, kinds_))
+    wide = {"bf16": rounds * 2.0 ** -8, "f16": rounds * 2.0 ** -11, "f32": TOL["f32"]}
     tol = TOL[dtype] if kw.get("dist", "recipe") == "recipe" else max(TOL[dtype], wide[dtype])
     for r in range(P):
         assert np.array_equal(outs[r].view(np.uint8), tree[r].view(np.uint8)), f"rank {r} not bit-exact"
