@@ -252,6 +252,8 @@ def main():
               ((2, 4), (1, 1), "f32", 16, 1028, S.AR, th.THEMIS, "tma"),
               ((4, 2), (1, 1), "i32", 16, 1028, S.AR, th.THEMIS, "tma"),
               ((W,), (1,), "f32", 4, 8196, S.AR, th.THEMIS, "tma", (th.RING,)),
+              ((W,), (1,), "bf16", 4, 8200, S.AR, th.THEMIS, "tma", (th.RING,)),        # per-hop rounding (R18)
+              ((4, 2), (1, 1), "f16", 8, 2056, S.AR, th.THEMIS, "tma", (th.RING, th.DIRECT)),
               ((2, 2, 2), (1, 1, 1), "f32", 4, 4100, S.AR, th.THEMIS, "tma", (th.RING,) * 3),
               ((2, 4), (1, 1), "f32", 8, 2052, S.AR, th.THEMIS, "tma", (th.DIRECT, th.RING)),
               ((4, 2), (1, 1), "f32", 8, 2052, "RS", th.THEMIS, "tma", (th.RING, th.DIRECT))]
