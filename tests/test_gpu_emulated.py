@@ -539,3 +539,39 @@ def test_random_executor_configs():
         except AssertionError as e:
             raise AssertionError(f"case {i}: sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy} "
                                  f"intra {intra} conc {conc} mcb {mcb} slice {slice_elems} ctas {ctas}: {e}")
+
+
+def test_random_rs_ag_configs():
+    """Randomised RS / AG halves (N = 1): 24 random (topology, kinds, BW,
+    dtype, chunks, policy) — RS block r and the full AG buffer bit-exact
+    against the oracle's schedule, int32 also against the plain definitions."""
+    import random
+    rng = random.Random(2110)
+    for i in range(24):
+        D = rng.randint(1, 3)
+        sizes = tuple(rng.choice([2, 3, 4]) for _ in range(D))
+        kinds = tuple(rng.choice([th.DIRECT, th.RING]) for _ in range(D))
+        bw = tuple(rng.choice([1, 2, 4]) for _ in range(D))
+        dtype = rng.choice(["i32", "f32", "bf16", "f16"])
+        C_ = rng.choice([1, 2, 4, 8])
+        policy = rng.choice([th.THEMIS, th.BASELINE])
+        coll = rng.choice(["RS", "AG"])
+        slice_elems = (16 // ELEM_SIZE[dtype]) * rng.randint(1, 500)
+        xs, outs = run_case(sizes, bw, dtype, C_, slice_elems, coll, policy, kinds=kinds,
+                            dist="wide" if dtype != "i32" else "recipe")
+        P, N = len(xs), xs[0].shape[0]
+        sched = oracle_sched(sizes, bw, coll, N * ELEM_SIZE[dtype], C_, policy, kinds=kinds)
+        tree = O.run_schedule(xs, sched, dtype)
+        blk = N // P
+        msg = f"case {i}: {coll} sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy}"
+        for r in range(P):
+            got = outs[r][r * blk:(r + 1) * blk] if coll == "RS" else outs[r]
+            want = tree[r][r * blk:(r + 1) * blk] if coll == "RS" else tree[r]
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), msg + f" rank {r}"
+        if dtype == "i32":
+            if coll == "RS":
+                d = O.reduce_scatter_definition(xs, "i32", P)
+                assert all(np.array_equal(outs[r][r * blk:(r + 1) * blk], d[r]) for r in range(P)), msg
+            else:
+                cat = O.all_gather_definition(xs, P)
+                assert all(np.array_equal(outs[r], cat) for r in range(P)), msg
