@@ -257,6 +257,17 @@ def main():
               ((2, 2, 2), (1, 1, 1), "f32", 4, 4100, S.AR, th.THEMIS, "tma", (th.RING,) * 3),
               ((2, 4), (1, 1), "f32", 8, 2052, S.AR, th.THEMIS, "tma", (th.DIRECT, th.RING)),
               ((4, 2), (1, 1), "f32", 8, 2052, "RS", th.THEMIS, "tma", (th.RING, th.DIRECT))]
+    import random
+    rng = random.Random(4478 + W)            # identical on every rank
+    for _ in range(12):                      # randomised cases (every rank draws the same)
+        D = rng.randint(1, 3)
+        sizes = tuple(rng.choice([2, 2, 4]) for _ in range(D))
+        kinds = tuple(rng.choice([th.DIRECT, th.RING]) for _ in range(D))
+        dtype = rng.choice(["i32", "f32", "bf16", "f16"])
+        vec = 16 // ELEM_SIZE[dtype]
+        cases.append((sizes, tuple(rng.choice([1, 2, 4]) for _ in range(D)), dtype, rng.choice([1, 4, 8]),
+                      vec * rng.randint(1, 300), rng.choice([S.AR, S.AR, "RS", "AG"]),
+                      rng.choice([th.THEMIS, th.BASELINE]), "tma", kinds))
     fails = []
     for c in cases:
         if int(np.prod(c[0])) % W:
