@@ -148,7 +148,7 @@ def config4(r: Runner, quick):
         buckets = bucket_sizes(nparams, 2)
         if quick:
             buckets = buckets[:3] + buckets[-1:]
-        maxc = pad_count(max(buckets), P, C, 2)
+        maxc = pad_count(max(buckets), P, th.AUTO_MAX_CHUNKS, 2)     # room for every chunk-count candidate
         comm = r.comm(sizes, maxc * 2)
         for rat in [(1, 1, 1), (4, 2, 1)]:
             for mode in ("caps", "paced"):
@@ -167,6 +167,20 @@ def config4(r: Runner, quick):
                         tot += sec
                         per.append(round(2 * cnt * 2 * (P - 1) / P / sec / 1e9, 1))
                     res[name] = {"total_ms": round(tot * 1e3, 3), "bucket_bus_gbs": per}
+                if LAT and mode == "paced":   # latency-aware Themis, planner-chosen chunks (R25)
+                    tot, per, chosen = 0.0, [], []
+                    t = th.Topology(sizes, bw, None, (LAT,) * len(sizes))
+                    for n in buckets:
+                        cnt = pad_count(n, P, th.AUTO_MAX_CHUNKS, 2)
+                        plan = th.Plan(t, th.ALLREDUCE, cnt * 2, th.AUTO_CHUNKS, th.THEMIS, th.SCF,
+                                       charge_latency=True)
+                        plan.bind(comm, th.default_ctas(rat, r.ctas_total))
+                        sec = r.time(comm, plan, th.ALLREDUCE, cnt, "bf16", steps=2, warmup=1)
+                        chosen.append(plan.n_chunks)
+                        plan.close()
+                        tot += sec
+                        per.append(round(2 * cnt * 2 * (P - 1) / P / sec / 1e9, 1))
+                    res["themis_auto"] = {"total_ms": round(tot * 1e3, 3), "bucket_bus_gbs": per, "chunks": chosen}
                 r.emit({"config": 4, "n_gpus": r.world, "model": model, "params": nparams, "buckets": len(buckets),
                         "bucket_elems": buckets, "ratio": ":".join(map(str, rat)), "mode": mode, **res,
                         "speedup": round(res["baseline"]["total_ms"] / res["themis"]["total_ms"], 3)})
