@@ -53,6 +53,8 @@ def main():
     ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
     ap.add_argument("--chunks", type=int, default=64)
     ap.add_argument("--concurrency", type=int, default=1)
+    ap.add_argument("--latency-ns", type=int, default=0,
+                    help="also run latency-aware Themis plans with planner-chosen chunks (measured A_K, ns)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     a = ap.parse_args()
@@ -81,12 +83,13 @@ def main():
     for model in models:
         buckets = bucket_sizes(WORKLOAD_PARAMS[model], 2)
         counts = [pad_count(n, P, a.chunks, 2) for n in buckets]
-        comm = th.Comm(th.Topology(sizes, bw), max(counts) * 2, group=group, device=local)
+        counts_auto = [pad_count(n, P, th.AUTO_MAX_CHUNKS, 2) for n in buckets]
+        comm = th.Comm(th.Topology(sizes, bw), max(counts + counts_auto) * 2, group=group, device=local)
         comm.set_timeout(60.0)
         comm.set_stages(4 if ncross else 6)
         comm.set_pacing(a.paced)
         for v in range(V):
-            comm.rank_view(v, max(counts), "bf16").normal_(0, 1e-2)
+            comm.rank_view(v, max(counts + counts_auto), "bf16").normal_(0, 1e-2)
         # per-bucket GEMM: 2 * MN * MN * k = V * 4 * params * tokens
         ks = [max(64, int(V * 4 * n * TOKENS[model] / (2 * GEMM_MN * GEMM_MN)) // 64 * 64) for n in buckets]
         A = torch.randn(GEMM_MN, max(ks), device=dev, dtype=torch.bfloat16)
@@ -97,11 +100,20 @@ def main():
                "n_gpus": world, "ranks_per_gpu": V, "ratio": a.ratio, "mode": "paced" if a.paced else "caps",
                "bw_mbps": list(bw) if a.paced else None, "ctas_total": ctas_total,
                "compute_tflop_per_gpu": round(flops / 1e12, 3), "concurrency": a.concurrency}
-        for pol, name in ((th.BASELINE, "baseline"), (th.THEMIS, "themis")):
+        variants = [(th.BASELINE, "baseline"), (th.THEMIS, "themis")]
+        if a.latency_ns:
+            variants.append((th.THEMIS, "themis_auto"))
+        for pol, name in variants:
             plans = {}
-            for c in sorted(set(counts)):
-                p = th.Plan(th.Topology(sizes, bw), th.ALLREDUCE, c * 2, a.chunks, pol,
-                            th.SCF if pol == th.THEMIS else th.FIFO, concurrency=a.concurrency)
+            auto = name == "themis_auto"
+            cnts = counts_auto if auto else counts
+            for c in sorted(set(cnts)):
+                if auto:    # latency-aware, planner-chosen chunk count (R25)
+                    t = th.Topology(sizes, bw, None, (a.latency_ns,) * len(sizes))
+                    p = th.Plan(t, th.ALLREDUCE, c * 2, th.AUTO_CHUNKS, th.THEMIS, th.SCF, charge_latency=True)
+                else:
+                    p = th.Plan(th.Topology(sizes, bw), th.ALLREDUCE, c * 2, a.chunks, pol,
+                                th.SCF if pol == th.THEMIS else th.FIFO, concurrency=a.concurrency)
                 plans[c] = p.bind(comm, th.default_ctas(rat, ctas_total))
 
             def iteration(do_comp, do_comm):
@@ -116,7 +128,7 @@ def main():
                     if do_comm:
                         if do_comp:
                             comm_stream.wait_event(ev[-1])
-                        th.run(th.ALLREDUCE, comm, plans[counts[i]], counts[i], "bf16", comm_stream)
+                        th.run(th.ALLREDUCE, comm, plans[cnts[i]], cnts[i], "bf16", comm_stream)
 
             def timed(do_comp, do_comm):
                 ts = []
@@ -145,6 +157,8 @@ def main():
             for p in plans.values():
                 p.close()
         row["iteration_speedup"] = round(row["baseline"]["iteration_ms"] / row["themis"]["iteration_ms"], 3)
+        if "themis_auto" in row:
+            row["auto_iteration_speedup"] = round(row["baseline"]["iteration_ms"] / row["themis_auto"]["iteration_ms"], 3)
         row["comm_speedup"] = round(row["baseline"]["comm_only_ms"] / row["themis"]["comm_only_ms"], 3)
         if rank == 0:
             os.write(out_fd, (json.dumps(row) + "\n").encode())
