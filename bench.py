@@ -271,6 +271,19 @@ def run_themis(a):
                     # the plan's makespan is in real ns here (absolute bw): model busBW / sum BW
                     row["model_util"] = {n: round(busbw(row[n]["model_makespan_ns"] * 1e-9) / sum_bw, 4)
                                          for n in ("baseline", "themis")}
+                    # latency-aware Themis with a planner-chosen chunk count (R25; A_K as measured
+                    # by scripts/calibrate.py) beside the fixed 64-chunk plans
+                    lat = a.latency_ns or (8500 if not lay["cross_gpu_dims"] else 11000)
+                    pa = th.Plan(th.Topology(SIZES, paced_bw(rat, pace_gbs), None, (lat,) * len(SIZES)),
+                                 th.ALLREDUCE, S, th.AUTO_CHUNKS, th.THEMIS, th.SCF, charge_latency=True)
+                    check_same_plan(pa, group)
+                    pa.bind(comm, caps_for(rat))
+                    ta = timed(pa, max(2, min(a.steps, 5)), 1)[0]
+                    row["themis_auto"] = {"bus_gbs": round(busbw(ta), 1), "ms": round(ta * 1e3, 3),
+                                          "chunks": pa.n_chunks, "latency_ns": lat,
+                                          "util": round(busbw(ta) / sum_bw, 4)}
+                    row["auto_speedup"] = round(row["baseline"]["ms"] / row["themis_auto"]["ms"], 3)
+                    pa.close()
                 compare[f"{mode} {':'.join(map(str, rat))}"] = row
         comm.set_pacing(False)
 
@@ -542,6 +555,8 @@ def main():
     ap.add_argument("--ratio", default="4:2:1", help="emulated BW(dim1):BW(dim2):BW(dim3)")
     ap.add_argument("--ctas-total", type=int, default=0, help="CTAs split over the dims (default: all SMs)")
     ap.add_argument("--ctas-split", default="", help="explicit CTAs per dim for the headline ratio (experiments)")
+    ap.add_argument("--latency-ns", type=int, default=0,
+                    help="per-op A_K for the latency-aware auto-chunk compare rows (default: measured 8.5 / 11 us)")
     ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")
     ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
     ap.add_argument("--no-compare", action="store_true")
