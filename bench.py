@@ -521,9 +521,12 @@ def run_reference(a):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": "BASELINE.json configs[1] (2x2x2, fp32, 64 chunks, 4:2:1) — bounded sample of "
-                                  f"{a.cpu_mib} MiB per rank on the host CPU", "topology": "x".join(map(str, SIZES)),
-                      "bytes_per_rank": N * 4, "chunks": a.chunks, "bw_ratio": a.ratio},
+           "config": {"workload": "BASELINE.json configs[1]: 2x2x2 logical topology, 1 GiB fp32 All-Reduce per "
+                                  "rank, 64 chunks, emulated per-dim BW 4:2:1",
+                      "topology": "x".join(map(str, SIZES)), "bytes_per_rank": a.mib << 20, "chunks": a.chunks,
+                      "bw_ratio": a.ratio, "policy": "themis+scf",
+                      "sample": f"each step is a bounded sample: {a.cpu_mib} MiB fp32 per rank x {P} simulated ranks "
+                                "on the host CPU (numpy, one core)", "sample_bytes_per_rank": N * 4},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
                             "sample": f"{a.cpu_mib} MiB fp32 per rank x {P} simulated ranks per step"},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
