@@ -194,6 +194,9 @@ themis_status_t themis_heap_close(void* peer_heap /*[device]*/);
 themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, const themis_topology_t* topo /*[host]*/,
                                    void* const* heaps /*[host] n_gpus UVA pointers*/, uint64_t heap_bytes,
                                    uint64_t vrank_stride, themis_comm_t** out /*[out]*/);
+/* Frees the comm's device state (waits for its host-stream copies).  Plans
+ * still bound to it are unbound (themis_plan_bind them again to reuse them);
+ * the heaps stay the caller's (themis_heap_free / themis_heap_close). */
 void themis_comm_free(themis_comm_t* comm);
 /* Latched asynchronous device errors (THEMIS_ERR_TIMEOUT) or THEMIS_OK.
  * Non-blocking: reads a host-mapped error word the kernel writes. */

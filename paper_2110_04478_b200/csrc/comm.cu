@@ -94,6 +94,7 @@ struct themis_comm {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   uint32_t* d2h_flags = nullptr;  // [THEMIS_MAX_CHUNKS] device
   uint32_t host_seq = 0;
+  std::vector<themis_plan_t*> bound;  // plans bound to this comm (unbound when it is freed)
 };
 
 namespace themis {
@@ -216,8 +217,11 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   return THEMIS_OK;
 }
 
+static void free_bind(themis_plan_t* pl);
+
 extern "C" void themis_comm_free(themis_comm_t* c) {
   if (!c) return;
+  while (!c->bound.empty()) free_bind(c->bound.back());  // a plan may outlive its comm: unbind it
   if (c->h2d) {
     cudaStreamSynchronize(c->h2d);
     cudaStreamSynchronize(c->d2h);
@@ -298,6 +302,8 @@ extern "C" themis_status_t themis_trace_fetch_detail(themis_comm_t* c, uint64_t*
 
 static void free_bind(themis_plan_t* pl) {
   if (!pl->bind) return;
+  auto& v = pl->bind->comm->bound;
+  v.erase(std::remove(v.begin(), v.end(), pl), v.end());
   cudaFree(pl->bind->d_ops);
   cudaFree(pl->bind->d_dim_ops);
   delete pl->bind;
@@ -441,6 +447,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   }
   b->total_ctas = tot;
   pl->bind = b;
+  c->bound.push_back(pl);
   return THEMIS_OK;
 }
 

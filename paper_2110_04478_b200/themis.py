@@ -413,13 +413,19 @@ class Comm:
         for p in self.__dict__.pop("_plans", {}).values():
             p.close()
         if getattr(self, "h", None):
-            lib().themis_comm_free(self.h)
+            lib().themis_comm_free(self.h)      # also unbinds any plan still bound to it
             self.h = None
             for p in self.imported:
                 lib().themis_heap_close(p)
             self.imported = []
             lib().themis_heap_free(self.heap)
             self.heap = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _stream_ptr(stream):

@@ -575,3 +575,30 @@ def test_random_rs_ag_configs():
             else:
                 cat = O.all_gather_definition(xs, P)
                 assert all(np.array_equal(outs[r], cat) for r in range(P)), msg
+
+
+def test_plan_outlives_comm():
+    """A plan bound to a comm that is closed first is unbound (not dangling):
+    running it reports PLAN_MISMATCH ("not bound"); rebinding to a new comm works."""
+    topo = th.Topology((2, 2), (1, 1))
+    N = 4 * 4 * 1024
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, 4)
+    comm = th.Comm(topo, N * 4)
+    plan.bind(comm)
+    ptr = comm.data_ptr
+    comm.close()
+    with pytest.raises(th.ThemisError) as e:
+        th.themis_allreduce(ptr, N, "i32", plan)
+    assert e.value.status == 6
+    comm2 = th.Comm(topo, N * 4)
+    try:
+        plan.bind(comm2)
+        xs = host_inputs(4, N, "i32")
+        for r in range(4):
+            comm2.rank_view(r, N, "i32").copy_(torch.from_numpy(xs[r]))
+        th.run(th.ALLREDUCE, comm2, plan, N, "i32")
+        torch.cuda.synchronize()
+        assert np.array_equal(comm2.rank_view(2, N, "i32").cpu().numpy(), O.allreduce_definition(xs, "i32"))
+    finally:
+        plan.close()
+        comm2.close()
