@@ -60,6 +60,26 @@ class Topology:
         return t
 
 
+def _table2(sizes, gbps_per_link, links, latency_ns, kinds) -> Topology:
+    """Aggregate per-NPU BW of a dim = Gb/s per link x links / 8 (GB/s) -> MB/s."""
+    return Topology(tuple(sizes), tuple(b * n * 125 for b, n in zip(gbps_per_link, links)), tuple(kinds),
+                    tuple(latency_ns))
+
+
+# PAPER.md Table 2 (:509-519): the paper's simulated platforms (planner use;
+# 1024 NPUs): sizes, BW per link (Gb/s), links per NPU, step latency (ns), Table 1 kind.
+TABLE2 = {
+    "2D-SW_SW": _table2((16, 64), (200, 800), (6, 1), (700, 1700), (SWITCH, SWITCH)),
+    "3D-SW_SW_SW_homo": _table2((16, 8, 8), (200, 200, 800), (4, 4, 1), (700, 700, 1700), (SWITCH,) * 3),
+    "3D-SW_SW_SW_hetero": _table2((16, 8, 8), (200, 200, 400), (8, 4, 1), (700, 700, 1700), (SWITCH,) * 3),
+    "3D-FC_Ring_SW": _table2((8, 16, 8), (200, 200, 400), (7, 4, 1), (700, 700, 1700), (DIRECT, RING, SWITCH)),
+    "4D-Ring_SW_SW_SW": _table2((4, 4, 8, 8), (1000, 200, 200, 400), (2, 8, 4, 1), (20, 700, 700, 1700),
+                                (RING, SWITCH, SWITCH, SWITCH)),
+    "4D-Ring_FC_Ring_SW": _table2((4, 8, 4, 8), (1500, 200, 200, 800), (2, 7, 6, 1), (20, 700, 700, 1700),
+                                  (RING, DIRECT, RING, SWITCH)),
+}
+
+
 def themis_plan(topo: Topology, coll: int, nbytes: int, n_chunks: int, policy: int = THEMIS, intra: int = SCF,
                 threshold_div: int = 16, charge_latency: bool = False, concurrency: int = 1,
                 chunk_release_ns: int = 0) -> C.c_void_p:

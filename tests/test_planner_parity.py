@@ -327,3 +327,16 @@ def test_csv_export_matches_oracle(coll):
             assert plan.to_csv() == S.export_csv(sched)
         finally:
             plan.close()
+
+
+def test_table2_presets_in_the_binding():
+    """The binding's TABLE2 presets equal the oracle's transcription of
+    PAPER.md Table 2 (sizes, aggregate BW, kinds, latencies), and a Themis plan
+    on each is bit-identical to the oracle's."""
+    for name, g in th.TABLE2.items():
+        o = T.PRESETS[name]
+        assert g.sizes == tuple(d.size for d in o.dims)
+        assert [Fraction(b, 1000) for b in g.bw_mbps] == [d.bw for d in o.dims]
+        assert [KINDS[d.kind] for d in o.dims] == list(g.kinds)
+        assert [Fraction(x) for x in g.latency_ns] == [d.step_latency for d in o.dims]
+        compare(o, g, S.AR, 1 << 30, 16, S.THEMIS, E.SCF)
