@@ -181,6 +181,13 @@ class Plan:
             lines.append(f"{c},{r},{a},{cb}")
         return "\n".join(lines) + "\n"
 
+    def utilization(self) -> Fraction:
+        """The paper's average BW utilisation of the pre-simulated run,
+        sum_K BW_K busy_K / (sum BW * makespan) (R14), exact."""
+        bw = [int(b) for b in self.topo.bw_mbps]
+        busy = self.info["busy"]
+        return Fraction(sum(b * t for b, t in zip(bw, busy)), sum(bw) * self.info["makespan"])
+
     def makespan_ns(self) -> Fraction:
         return Fraction(self.info["makespan"], self.info["time_scale"])
 

@@ -340,3 +340,17 @@ def test_table2_presets_in_the_binding():
         assert [KINDS[d.kind] for d in o.dims] == list(g.kinds)
         assert [Fraction(x) for x in g.latency_ns] == [d.step_latency for d in o.dims]
         compare(o, g, S.AR, 1 << 30, 16, S.THEMIS, E.SCF)
+
+
+def test_plan_utilization_matches_oracle():
+    """Plan.utilization() == the oracle's util (R14) exactly, both policies."""
+    for sizes, bw in (((2, 2, 2), (100000, 100000, 100000)), ((4, 2), (200000, 50000)), ((16, 8, 8), (100000, 100000, 50000))):
+        o, g = make_pair(sizes, bw)
+        for pol in (S.BASELINE, S.THEMIS):
+            m = E.simulate(S.schedule_collective(o, S.AR, 1 << 28, 32, pol), E.SCF if pol == S.THEMIS else E.FIFO)
+            plan = th.Plan(g, th.ALLREDUCE, 1 << 28, 32, th.THEMIS if pol == S.THEMIS else th.BASELINE,
+                           th.SCF if pol == S.THEMIS else th.FIFO)
+            try:
+                assert plan.utilization() == m.util
+            finally:
+                plan.close()
