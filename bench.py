@@ -164,16 +164,17 @@ def run_themis(a):
         total_ctas = a.ctas_total
     elif ncross_ == 0:
         total_ctas = sms
-    elif ncross_ == len(SIZES):   # every dim over NVLink (calibration: 2x2 best at 96 CTAs x 3 stages)
-        total_ctas = min(sms, 32 * len(SIZES) + 32) if len(SIZES) > 1 else 32
+    elif ncross_ == len(SIZES):   # every dim over NVLink (calibration: 2x2 best at 128 CTAs x 2 x 32 KiB)
+        total_ctas = min(sms, 128) if len(SIZES) > 1 else 32
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
     # TMA ring (stages x stage bytes, <= 192 KiB): larger tiles cut the fixed
     # per-tile cost (profiles/r01/stagekb/: 3 x 64 KiB +0.8 % at N = 1, 4 x 48
-    # KiB +2 % at N = 4 over 6 x 32); all-NVLink topologies want fewer bytes in
-    # flight per GPU (calibration above: 3 x 32 KiB)
+    # KiB +2 % at N = 4 over 6 x 32); all-NVLink topologies peak with ~8 MB in
+    # flight per GPU, spread over many CTAs (scripts/allnvlink_sweep.sh: 128 CTAs
+    # x 2 x 32 KiB 627 vs 96 x 3 x 32 KiB 600 GB/s on 2x2)
     if ncross_ == len(SIZES):
-        stages, stage_kb = a.stages or (3 if len(SIZES) > 1 else 4), a.stage_kb or 32
+        stages, stage_kb = a.stages or (2 if len(SIZES) > 1 else 4), a.stage_kb or 32
     elif ncross_ == 0:
         stages, stage_kb = a.stages or 3, a.stage_kb or 64
     else:

@@ -51,8 +51,8 @@ class Runner:
         c.set_timeout(30.0)
         lay = bench.logical_layout(sizes, self.world)
         ncross = len(lay["cross_gpu_dims"])
-        c.set_stages(6 if ncross < len(sizes) else (3 if len(sizes) > 1 else 4))
-        self.ctas_total = self.sms if ncross == 0 else (32 if ncross == len(sizes) else
+        c.set_stages(6 if ncross < len(sizes) else (2 if len(sizes) > 1 else 4))
+        self.ctas_total = self.sms if ncross == 0 else ((min(self.sms, 128) if len(sizes) > 1 else 32) if ncross == len(sizes) else
                                                           (self.sms if lay["V"] >= 4 else 96))
         self.V = lay["V"]
         return c
