@@ -514,9 +514,10 @@ def test_random_executor_configs():
     dtype, chunks, policy, intra, concurrency, op windows, CTA caps) — every
     output bit-exact against the oracle run with the same schedule (int32
     against the plain definition)."""
+    import os
     import random
-    rng = random.Random(4478)
-    for i in range(40):
+    rng = random.Random(int(os.environ.get("THEMIS_RANDOM_SEED", 4478)))
+    for i in range(int(os.environ.get("THEMIS_RANDOM_CASES", 40))):
         D = rng.randint(1, 4)
         sizes = [rng.choice([2, 2, 3, 4]) for _ in range(D)]
         while int(np.prod(sizes)) > 32:
@@ -545,9 +546,10 @@ def test_random_rs_ag_configs():
     """Randomised RS / AG halves (N = 1): 24 random (topology, kinds, BW,
     dtype, chunks, policy) — RS block r and the full AG buffer bit-exact
     against the oracle's schedule, int32 also against the plain definitions."""
+    import os
     import random
-    rng = random.Random(2110)
-    for i in range(24):
+    rng = random.Random(int(os.environ.get("THEMIS_RANDOM_SEED", 2110)))
+    for i in range(int(os.environ.get("THEMIS_RANDOM_CASES", 24))):
         D = rng.randint(1, 3)
         sizes = tuple(rng.choice([2, 3, 4]) for _ in range(D))
         kinds = tuple(rng.choice([th.DIRECT, th.RING]) for _ in range(D))
