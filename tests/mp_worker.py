@@ -258,8 +258,8 @@ def main():
               ((2, 4), (1, 1), "f32", 8, 2052, S.AR, th.THEMIS, "tma", (th.DIRECT, th.RING)),
               ((4, 2), (1, 1), "f32", 8, 2052, "RS", th.THEMIS, "tma", (th.RING, th.DIRECT))]
     import random
-    rng = random.Random(4478 + W)            # identical on every rank
-    for _ in range(12):                      # randomised cases (every rank draws the same)
+    rng = random.Random(int(os.environ.get("THEMIS_RANDOM_SEED", 4478)) + W)   # identical on every rank
+    for _ in range(int(os.environ.get("THEMIS_MP_RANDOM", 12))):               # randomised cases
         D = rng.randint(1, 3)
         sizes = tuple(rng.choice([2, 2, 4]) for _ in range(D))
         kinds = tuple(rng.choice([th.DIRECT, th.RING]) for _ in range(D))
