@@ -460,6 +460,9 @@ def run_themis(a):
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
                        "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages, "tma_stage_kib": stage_kb,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
+                       "scaling_note": ("the same 8-rank logical topology at every N: N = 1 emulates all ranks in "
+                                        "one GPU's HBM, N = 8 is one rank per GPU over NVLink (V = 8 / N ranks "
+                                        "per GPU); total work is fixed, hence 'strong'"),
                        "aggregate_bus_gbs": round(busbw(t_main) * P, 1),
                        "best_step_bus_gbs": round(busbw(t_best), 2),
                        "median_step_bus_gbs": round(busbw(t_median), 2),
