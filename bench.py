@@ -179,8 +179,9 @@ def run_themis(a):
         stages, stage_kb = a.stages or 3, a.stage_kb or 64
     else:
         stages, stage_kb = a.stages or 4, a.stage_kb or 48
-    topo = th.Topology(SIZES, ratio)
-    comm = th.Comm(topo, S, group=group, device=local)
+    kinds = (th.SWITCH,) * len(SIZES) if a.nvls else None   # NVSwitch dims: in-switch reduction where eligible (R27)
+    topo = th.Topology(SIZES, ratio, kinds)
+    comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
     comm.set_timeout(30.0)
     comm.set_stages(1)
     comm.set_stage_bytes(stage_kb * 1024)
@@ -195,7 +196,7 @@ def run_themis(a):
         # total_gbs: absolute per-rank bandwidth budget split in the ratio (paced
         # emulation); otherwise the ratio itself (only ratios matter to the plan).
         bw = paced_bw(rat, total_gbs) if total_gbs else rat
-        t = th.Topology(SIZES, bw)
+        t = th.Topology(SIZES, bw, kinds)
         p = th.Plan(t, th.ALLREDUCE, S, a.chunks, pol, th.SCF if pol == th.THEMIS else th.FIFO,
                     concurrency=a.concurrency)
         check_same_plan(p, group)            # fail fast before any kernel (R22)
@@ -275,7 +276,7 @@ def run_themis(a):
                     # latency-aware Themis with a planner-chosen chunk count (R25; A_K as measured
                     # by scripts/calibrate.py) beside the fixed 64-chunk plans
                     lat = a.latency_ns or (8500 if not lay["cross_gpu_dims"] else 11000)
-                    pa = th.Plan(th.Topology(SIZES, paced_bw(rat, pace_gbs), None, (lat,) * len(SIZES)),
+                    pa = th.Plan(th.Topology(SIZES, paced_bw(rat, pace_gbs), kinds, (lat,) * len(SIZES)),
                                  th.ALLREDUCE, S, th.AUTO_CHUNKS, th.THEMIS, th.SCF, charge_latency=True)
                     check_same_plan(pa, group)
                     pa.bind(comm, caps_for(rat))
@@ -382,11 +383,11 @@ def run_themis(a):
         release_ns = int(V * S / a.chunks / h2d_gbs)
         bw_abs = paced_bw(ratio, max(24.0, busbw(t_main)))
         try:
-            hplan = th.Plan(th.Topology(SIZES, bw_abs), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
+            hplan = th.Plan(th.Topology(SIZES, bw_abs, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
                             concurrency=a.concurrency, chunk_release_ns=release_ns)
         except th.ThemisError:       # (planner overflow) all chunks ready at 0 instead
             release_ns = 0
-            hplan = th.Plan(th.Topology(SIZES, ratio), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
+            hplan = th.Plan(th.Topology(SIZES, ratio, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF,
                             concurrency=a.concurrency)
         check_same_plan(hplan, group)
         hplan.bind(comm, caps_for(ratio))
@@ -562,6 +563,8 @@ def main():
     ap.add_argument("--ratio", default="4:2:1", help="emulated BW(dim1):BW(dim2):BW(dim3)")
     ap.add_argument("--ctas-total", type=int, default=0, help="CTAs split over the dims (default: all SMs)")
     ap.add_argument("--ctas-split", default="", help="explicit CTAs per dim for the headline ratio (experiments)")
+    ap.add_argument("--nvls", action="store_true",
+                    help="switch dims + multicast heap: eligible dims reduce in the NVSwitch (experimental, R27)")
     ap.add_argument("--latency-ns", type=int, default=0,
                     help="per-op A_K for the latency-aware auto-chunk compare rows (default: measured 8.5 / 11 us)")
     ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")

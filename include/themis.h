@@ -233,6 +233,16 @@ themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t byte
  * small op occupies (and synchronises) only the CTAs it needs.  Takes effect at
  * the next themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rotate);
+/* NVLS (in-switch reduction): mc_heap [device] = the
+ * multicast (NVSwitch) mapping of this GPU's heap, at the same offsets, bound
+ * on all W GPUs (e.g. torch symmetric memory's multicast pointer); NULL = off.
+ * At the next themis_plan_bind, on every THEMIS_DIM_SWITCH dim whose group is
+ * one rank per GPU at the same local index (P_k == W, stride_k == V), an RS op
+ * directly followed by the chunk's AG op on that dim runs as one in-switch
+ * All-Reduce of the rank's piece (multimem.ld_reduce + multimem.st; the switch
+ * sums in its own order, bf16/f16 accumulate in fp32 and round once; R27).
+ * TMA engine only.  Errors: INVALID_ARG. */
+themis_status_t themis_comm_set_multicast(themis_comm_t* comm, void* mc_heap);
 /* Watchdog: spin-waits give up after timeout_ns (default 20 s) and latch TIMEOUT. */
 themis_status_t themis_comm_set_timeout(themis_comm_t* comm, uint64_t timeout_ns);
 /* Trace: when enabled, each dim group records %globaltimer start/end of every

@@ -95,6 +95,7 @@ struct themis_comm {
   uint32_t* d2h_flags = nullptr;  // [THEMIS_MAX_CHUNKS] device
   uint32_t host_seq = 0;
   std::vector<themis_plan_t*> bound;  // plans bound to this comm (unbound when it is freed)
+  char* mc_heap = nullptr;             // NVLS multicast mapping of the heap (themis_comm_set_multicast)
 };
 
 namespace themis {
@@ -105,6 +106,7 @@ struct BindState {
   int32_t grp_start[THEMIS_MAX_DIMS + 1] = {};
   int32_t ctas[THEMIS_MAX_DIMS] = {};
   int32_t total_ctas = 0;
+  bool nvls = false;  // some op runs through the switch (TMA engine only)
 };
 }  // namespace themis
 
@@ -252,6 +254,11 @@ extern "C" themis_status_t themis_comm_set_engine(themis_comm_t* c, int32_t engi
   c->engine = engine;
   return THEMIS_OK;
 }
+extern "C" themis_status_t themis_comm_set_multicast(themis_comm_t* c, void* mc_heap) {
+  if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
+  c->mc_heap = static_cast<char*>(mc_heap);
+  return THEMIS_OK;
+}
 extern "C" themis_status_t themis_comm_set_window_rotation(themis_comm_t* c, int32_t rotate) {
   if (!c || rotate < 0 || rotate > 1) return fail(THEMIS_ERR_INVALID_ARG, "rotate must be 0 or 1");
   c->window_rotate = rotate;
@@ -381,6 +388,31 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     d.ring = pl->topo.kind[o.dim] == THEMIS_DIM_RING && pl->topo.size[o.dim] >= 3;
     ops[i] = d;
   }
+  // NVLS (R27): on a switch dim whose group is one rank per GPU at the same
+  // local index (P_k == W, stride_k == V) and a comm with a multicast mapping,
+  // an RS op immediately followed by the chunk's AG op on the same dim runs as
+  // one in-switch All-Reduce of the own piece (multimem.ld_reduce + multimem.st);
+  // the AG op then only carries the dependency.
+  bool any_nvls = false;
+  if (c->mc_heap) {
+    int64_t stride = 1;
+    bool elig[THEMIS_MAX_DIMS] = {};
+    for (int k = 0; k < D; ++k) {
+      elig[k] = pl->topo.kind[k] == THEMIS_DIM_SWITCH && pl->topo.size[k] == c->W && stride == c->V && c->W > 1;
+      stride *= pl->topo.size[k];
+    }
+    for (int ch = 0; ch < pl->C; ++ch)
+      for (int st = 0; st + 1 < pl->NS; ++st) {
+        const size_t i = (size_t)ch * pl->NS + st;
+        const Op& a = pl->ops[i];
+        const Op& b = pl->ops[i + 1];
+        if (elig[a.dim] && a.phase == 0 && b.phase == 1 && b.dim == a.dim) {
+          ops[i].nvls = 1;
+          ops[i + 1].nvls = 2;
+          any_nvls = true;
+        }
+      }
+  }
   std::vector<int32_t> lists((size_t)D * pl->C * pl->NS, 0);
   for (int k = 0; k < D; ++k)
     for (size_t i = 0; i < pl->dim_ops[k].size(); ++i) {
@@ -446,6 +478,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     b->grp_start[k + 1] = b->grp_start[k] + n[k];
   }
   b->total_ctas = tot;
+  b->nvls = any_nvls;
   pl->bind = b;
   c->bound.push_back(pl);
   return THEMIS_OK;
@@ -540,6 +573,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.ag_rr = c->ag_rr;
   kp.host_seq = host_seq;
   kp.d2h_flags = c->d2h_flags;
+  kp.mc_heap = c->mc_heap;
   for (int k = 0; k < pl->D; ++k)  // ns per byte per CTA = c_k / (V * bw_k[bytes/ns])
     kp.pace_ns_per_byte[k] =
         c->pacing ? (float)((double)pl->bind->ctas[k] * 1000.0 / ((double)c->V * pl->topo.bw_mbps[k])) : 0.f;
@@ -549,6 +583,8 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
     for (int k = 0; k < pl->D; ++k)
       if (pl->topo.kind[k] == THEMIS_DIM_RING && pl->topo.size[k] >= 3)
         return fail(THEMIS_ERR_INVALID_ARG, "ring dimensions need the TMA engine (themis_comm_set_engine(comm, 1))");
+  if (!c->engine && pl->bind->nvls)
+    return fail(THEMIS_ERR_INVALID_ARG, "NVLS ops need the TMA engine (themis_comm_set_engine(comm, 1))");
   const void* fn = kernel_for(dtype, c->engine);
   if (c->trace_on) {  // op start = earliest working CTA (atomicMin over an all-ones start)
     cudaError_t m = cudaMemsetAsync(c->trace, 0xFF, 2 * kMaxOps * sizeof(uint64_t), static_cast<cudaStream_t>(stream));

@@ -277,6 +277,52 @@ __device__ __forceinline__ bool mbar_wait_or(uint64_t* bar, uint32_t parity, con
     if (*(volatile const uint32_t*)abort_flag) return false;
   }
 }
+// NVLS (NVSwitch in-switch reduction, PAPER.md:493-494 in-network offload):
+// 16 bytes reduced over every GPU bound to the multicast address, then the
+// result broadcast to all of them.  bf16 / f16 accumulate in fp32 in the
+// switch and round once; int32 wraps; the switch's summation order is its own.
+template <class Tag>
+__device__ __forceinline__ uint4 mc_ld_reduce(const void* mc);
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<F32Tag>(const void* mc) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<BF16Tag>(const void* mc) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<F16Tag>(const void* mc) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(mc) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<I32Tag>(const void* mc) {
+  const char* b = static_cast<const char*>(mc);
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.x) : "l"(b) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.y) : "l"(b + 4) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.z) : "l"(b + 8) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(v.w) : "l"(b + 12) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mc_st(void* mc, const uint4& v) {  // 16 bytes, bits as they are
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(mc), "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+                  "f"(__uint_as_float(v.w)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_token(uint64_t* bar) {  // a zero-byte "go" for a ring slot
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

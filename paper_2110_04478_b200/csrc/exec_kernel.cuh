@@ -19,7 +19,9 @@
 // A "unit" is one direct op or one ring step.
 
 constexpr int kMaxCtas = 160;  // CTAs per dimension group (ring step flags)
-enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3, U_DIRECT_AG_T = 4 };
+enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3, U_DIRECT_AG_T = 4,
+                U_NVLS = 5,   // fused NVLS All-Reduce of the own piece on a switch dim (RS op of an RS+AG pair)
+                U_NONE = 6 }; // its AG partner: no data (the NVLS broadcast delivered it), dependencies only
 
 // Per-op descriptor uploaded at bind (a5).
 struct OpDesc {
@@ -27,6 +29,7 @@ struct OpDesc {
   uint32_t reduced;                  // dims reduce-scattered before the op
   int32_t next_dim;                  // dim of stage+1 (-1: last stage)
   int32_t ring;                      // 1: ring algorithm on this dim
+  int32_t nvls;                      // 1: U_NVLS (fused RS+AG through the switch), 2: U_NONE (its AG partner)
   int32_t seq;                       // index of the op in its dim's enforced list
   int32_t width, offset;             // the op runs on CTAs [offset, offset+width) mod c_k of its group
   float pace_scale;                  // pacing: width / c_k for a lone narrow op (it gets the whole dim rate), else 1
@@ -66,6 +69,7 @@ struct KParams {
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
   uint32_t host_seq;        // host-buffer streaming (themis_allreduce_host): value of this call's h2d / d2h flags; 0 = off
   uint32_t* d2h_flags;      // [THEMIS_MAX_CHUNKS] device: chunk c final on this GPU (read by a stream wait op)
+  char* mc_heap;            // multicast (NVLS) mapping of this GPU's heap, same offsets; null = none
 };
 
 // ---------------------------------------------------------------- signal pads
@@ -178,6 +182,7 @@ __device__ __forceinline__ int unit_mode(const OpDesc& d) {
 // TMA path: a direct AG tile pulls the same offsets from all P_k - 1 peers at
 // once (U_DIRECT_AG_T), so every CTA keeps requests in flight to every peer.
 __device__ __forceinline__ int unit_mode_tma(const OpDesc& d) {
+  if (d.nvls) return d.nvls == 1 ? U_NVLS : U_NONE;
   const int m = unit_mode(d);
   return m == U_DIRECT_AG ? U_DIRECT_AG_T : m;
 }
@@ -215,7 +220,7 @@ __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, i
     f = it - vq * nblk;
     r.j = -1;
     const int ck = coord(p, r.q, k);
-    digit = mode == U_DIRECT_RS   ? ck
+    digit = (mode == U_DIRECT_RS || mode == U_NVLS) ? ck
           : mode == U_DIRECT_AG_T ? 0  // base: part j is at off + j * part_stride
           : mode == U_RING_RS     ? (ck + pk - 2 - step) % pk
                                   : ((ck - 1 - step) % pk + pk) % pk;
@@ -262,6 +267,7 @@ __device__ __forceinline__ void for_each_span(const KParams& p, const OpDesc& d,
 }
 
 __device__ __forceinline__ bool unit_has_work(const KParams& p, const OpDesc& d, int mode, int gi, int gn) {
+  if (mode == U_NONE) return gi == 0;  // one CTA carries the dependency wait
   const uint64_t Lb16 = p.slice_elems * p.elem_size / 16;
   if (mode == U_RING_RS || mode == U_RING_AG) {
     const uint64_t R16 = (uint64_t)d.nblk * Lb16;
@@ -339,6 +345,13 @@ __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { retu
 __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
                                              char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
                                              uint64_t t_op, double& sent) {
+  if (mode == U_NVLS || mode == U_NONE) {  // no TMA: a zero-byte token tells the consumers the deps hold
+    const int s = ctr % p.stages;
+    dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+    dev::mbar_arrive_token(&full[s]);
+    ++ctr;
+    return;
+  }
   const int nsrc = unit_nsrc(p, d, mode);
   const uint32_t tile = unit_tile(p, nsrc);
   const float pace = p.pace_ns_per_byte[d.dim] * d.pace_scale;
@@ -409,6 +422,21 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
   const uint32_t tile = unit_tile(p, nsrc), tile16 = tile / 16;
   const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
   bool ok = true;
+  if (mode == U_NVLS || mode == U_NONE) {  // consumers reduce through the switch directly (no ring data)
+    if (!unit_has_work(p, d, mode, gi, gn)) return true;
+    const int s = ctr % p.stages;
+    if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
+    if (mode == U_NVLS)
+      for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+        const Item m = decode_item(p, d, mode, step, it);
+        char* mc = p.mc_heap + p.data_rel + (uint64_t)(m.q % p.V) * p.vrank_stride + m.off;
+        for (uint64_t w = a / 16 + ct; w < e / 16; w += kCons) dev::mc_st(mc + 16 * w, dev::mc_ld_reduce<Tag>(mc + 16 * w));
+      });
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);
+    ++ctr;
+    return true;
+  }
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
     if (!ok) return;
     const Item m = decode_item(p, d, mode, step, it);

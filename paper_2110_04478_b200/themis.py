@@ -237,7 +237,9 @@ class Comm:
     per GPU; heaps are exchanged as CUDA IPC handles over the process group.
     """
 
-    def __init__(self, topo: Topology, data_bytes: int, group=None, device=None):
+    def __init__(self, topo: Topology, data_bytes: int, group=None, device=None, nvls: bool = False):
+        """nvls=True (W > 1): the heap is torch symmetric memory with an NVSwitch
+        multicast mapping, so switch dims can reduce in the switch (R27)."""
         import torch
         self.topo = topo
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -253,13 +255,28 @@ class Comm:
         self.P = topo.P
         self.V = topo.P // self.W
         self.sig_bytes, self.vrank_stride, self.heap_bytes = heap_layout(self.P, self.W, data_bytes)
-        heap = C.c_void_p()
-        check(lib().themis_heap_alloc(self.heap_bytes, C.byref(heap)))
-        self.heap = heap.value
         self.imported = []
+        self._symm = None
+        self.mc_heap = 0
         heaps = [0] * self.W
-        heaps[self.gpu_rank] = self.heap
-        if self.W > 1:
+        if nvls and self.W > 1:
+            import torch.distributed._symmetric_memory as symm
+            buf = symm.empty(self.heap_bytes, dtype=torch.uint8, device=self.device)
+            buf.zero_()
+            torch.cuda.synchronize(self.device)
+            hdl = symm.rendezvous(buf, group.group_name)
+            self.mc_heap = int(getattr(hdl, "multicast_ptr", 0) or 0)
+            if not self.mc_heap:
+                raise ThemisError(7, "NVLS requested but torch symmetric memory has no multicast mapping here")
+            self._symm = (buf, hdl)
+            heaps = [int(x) for x in hdl.buffer_ptrs]
+            self.heap = heaps[self.gpu_rank]
+        else:
+            heap = C.c_void_p()
+            check(lib().themis_heap_alloc(self.heap_bytes, C.byref(heap)))
+            self.heap = heap.value
+            heaps[self.gpu_rank] = self.heap
+        if self.W > 1 and self._symm is None:
             from .dist import allgather_bytes
             h = (C.c_uint8 * IPC_HANDLE_BYTES)()
             check(lib().themis_heap_export(self.heap, h))
@@ -279,6 +296,8 @@ class Comm:
                                        C.byref(out)))
         self.h = out
         self.data_ptr = self.heap + self.V * self.sig_bytes    # local rank 0's data region
+        if self.mc_heap:
+            check(lib().themis_comm_set_multicast(self.h, self.mc_heap))
 
     def rank_view(self, v: int, count: int, dtype: str):
         """torch view of local rank v's first `count` elements."""
@@ -445,7 +464,9 @@ class Comm:
             for p in self.imported:
                 lib().themis_heap_close(p)
             self.imported = []
-            lib().themis_heap_free(self.heap)
+            if self._symm is None:
+                lib().themis_heap_free(self.heap)
+            self._symm = None                    # torch frees the symmetric buffer
             self.heap = None
 
     def __del__(self):

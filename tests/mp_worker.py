@@ -217,6 +217,63 @@ def api_case(group, W, g):
     return bad
 
 
+def nvls_case(group, W, g):
+    """NVLS switch dims (R27) on a multicast heap: int32 exact vs the plain
+    definition; floats within the north_star tolerance of the fp64 sum (the
+    switch sums in its own order) and identical on every rank.  Returns the
+    number of mismatches (-1 if this box has no multicast)."""
+    SW, DI = th.SWITCH, th.DIRECT
+    cfgs = [((W,), (SW,), "i32", 8), ((W,), (SW,), "f32", 8), ((2, W), (DI, SW), "f32", 4),
+            ((2, W), (DI, SW), "bf16", 4)]
+    if W == 2:
+        cfgs.append(((2, 2, 2), (DI, DI, SW), "i32", 8))
+    bad = 0
+    for sizes, kinds, dtype, C in cfgs:
+        topo = th.Topology(sizes, (1,) * len(sizes), kinds)
+        P = topo.P
+        V = P // W
+        N = P * C * (16 // ELEM_SIZE[dtype]) * 257
+        try:
+            comm = th.Comm(topo, N * ELEM_SIZE[dtype], group=group, nvls=True)
+        except th.ThemisError:
+            return -1
+        comm.set_timeout(20.0)
+        plan = th.Plan(topo, th.ALLREDUCE, N * ELEM_SIZE[dtype], C).bind(comm)
+        xs = host_inputs(P, N, dtype)
+        for v in range(V):
+            src = torch.from_numpy(xs[g * V + v].view(np.int16) if dtype == "bf16" else xs[g * V + v])
+            comm.rank_view(v, N, dtype).copy_(src.view(torch.bfloat16) if dtype == "bf16" else src)
+        torch.cuda.synchronize()
+        for _ in range(2):                       # twice: the second call reduces the first's result
+            th.run(th.ALLREDUCE, comm, plan, N, dtype)
+        torch.cuda.synchronize()
+        comm.status()
+        outs = []
+        for v in range(V):
+            t = comm.rank_view(v, N, dtype).cpu()
+            outs.append(t.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else t.numpy())
+        once = O.allreduce_definition(xs, dtype)
+        if dtype == "i32":
+            want = O.allreduce_definition([once] * P, "i32")
+            bad += sum(not np.array_equal(o, want) for o in outs)
+        else:
+            want = P * once
+            scale = P * O.abs_sum(xs, dtype)
+            tol = {"f32": 1e-5, "bf16": 2e-2}[dtype]
+            bad += sum(not np.all(np.abs(O.to_f64(o, dtype) - want) <= tol * scale) for o in outs)
+        # every rank holds the same bits: compare a digest across GPUs
+        dig = torch.tensor([float(np.frombuffer(outs[0].tobytes(), np.uint8).astype(np.int64).sum() % 1000003)],
+                           device="cuda")
+        mx, mn = dig.clone(), dig.clone()
+        import torch.distributed as dist
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=group)
+        bad += int(mx.item() != mn.item()) + sum(not np.array_equal(o, outs[0]) for o in outs[1:])
+        plan.close()
+        comm.close()
+    return bad
+
+
 def fault_case(group, W, g):
     """Fault injection: rank 1 launches a plan
     with a different intra-dimension policy.  Every rank must report
@@ -280,6 +337,11 @@ def main():
         nb = api_case(group, W, rank)
         if nb:
             fails.append((("tensor API / host streaming / CUDA graph",), [f"{nb} mismatches"]))
+    nb = nvls_case(group, W, rank)
+    if nb > 0:
+        fails.append((("NVLS switch dims",), [f"{nb} mismatches"]))
+    elif nb < 0 and rank == 0:
+        print("mp_worker: NVLS cases skipped (no multicast on this box)")
     st = fault_case(group, W, rank)
     if st != 6:
         fails.append((("fault-injection plan mismatch",), [f"status {st}"]))
