@@ -430,7 +430,18 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
       for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
         const Item m = decode_item(p, d, mode, step, it);
         char* mc = p.mc_heap + p.data_rel + (uint64_t)(m.q % p.V) * p.vrank_stride + m.off;
-        for (uint64_t w = a / 16 + ct; w < e / 16; w += kCons) dev::mc_st(mc + 16 * w, dev::mc_ld_reduce<Tag>(mc + 16 * w));
+        // 4 independent in-switch reductions in flight per thread (the switch round trip is long)
+        constexpr int U = 4;
+        const uint64_t w0 = a / 16, w1 = e / 16;
+        uint64_t w = w0 + ct;
+        for (; w + (U - 1) * kCons < w1; w += U * kCons) {
+          uint4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = dev::mc_ld_reduce<Tag>(mc + 16 * (w + u * kCons));
+#pragma unroll
+          for (int u = 0; u < U; ++u) dev::mc_st(mc + 16 * (w + u * kCons), v[u]);
+        }
+        for (; w < w1; w += kCons) dev::mc_st(mc + 16 * w, dev::mc_ld_reduce<Tag>(mc + 16 * w));
       });
     __syncwarp();
     if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);
