@@ -165,7 +165,7 @@ def run_themis(a):
     elif ncross_ == 0:
         total_ctas = sms
     elif ncross_ == len(SIZES):   # every dim over NVLink (calibration: 2x2 best at 128 CTAs x 2 x 32 KiB)
-        total_ctas = min(sms, 128) if len(SIZES) > 1 else 32
+        total_ctas = min(sms, 128) if len(SIZES) > 1 else (64 if a.nvls else 32)   # NVLS wants more threads in flight
     else:   # mixed: GPU-local dims (HBM) want many CTAs
         total_ctas = sms if V >= 4 else 96
     # TMA ring (stages x stage bytes, <= 192 KiB): larger tiles cut the fixed
