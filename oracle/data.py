@@ -59,8 +59,11 @@ def _np_dtype(dtype: str):
 
 
 def reduce_hops(parts, dtype: str) -> np.ndarray:
-    """Ring dims (R18 amended): the partial travels the ring as a message in
-    the buffer's dtype, so it is rounded after every hop:
+    """Ring dims (R18): the executor sends ring messages in the buffer's dtype
+    (a design choice of the executor — PAPER.md is silent on message
+    precision; pinned against north_star's 1e-2 bound by
+    test_ring_low_precision_within_north_star_bound), so the tree-exact mode
+    rounds the partial after every hop:
     acc = parts[0]; acc = round(acc + parts[j]) for j = 1.. (fp32 adds)."""
     if dtype in ("f32", "i32", "f64"):
         return reduce_in_order(parts, dtype)       # storing the partial rounds nothing

@@ -259,7 +259,7 @@ def nvls_case(group, W, g):
         else:
             want = P * once
             scale = P * O.abs_sum(xs, dtype)
-            tol = {"f32": 1e-5, "bf16": 2e-2}[dtype]
+            tol = {"f32": 1e-5, "bf16": 1e-2}[dtype]   # north_star
             bad += sum(not np.all(np.abs(O.to_f64(o, dtype) - want) <= tol * scale) for o in outs)
         # every rank holds the same bits: compare a digest across GPUs
         dig = torch.tensor([float(np.frombuffer(outs[0].tobytes(), np.uint8).astype(np.int64).sum() % 1000003)],
