@@ -171,7 +171,7 @@ def run_themis(a):
     # TMA ring (stages x stage bytes, <= 192 KiB): larger tiles cut the fixed
     # per-tile cost (profiles/r01/stagekb/: 3 x 64 KiB +0.8 % at N = 1, 4 x 48
     # KiB +2 % at N = 4 over 6 x 32); all-NVLink topologies peak with ~8 MB in
-    # flight per GPU, spread over many CTAs (scripts/allnvlink_sweep.sh: 128 CTAs
+    # flight per GPU, spread over many CTAs (scripts/grid.py --preset hier-ring: 128 CTAs
     # x 2 x 32 KiB 627 vs 96 x 3 x 32 KiB 600 GB/s on 2x2)
     if ncross_ == len(SIZES):
         stages, stage_kb = a.stages or (2 if len(SIZES) > 1 else 4), a.stage_kb or 32

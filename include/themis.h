@@ -124,6 +124,14 @@ typedef struct {
   uint64_t dim_volume[THEMIS_MAX_DIMS]; /* N_K = sum_i n_K^i, x byte_scale */
   uint64_t final_load[THEMIS_MAX_DIMS]; /* Dim Load Tracker after the last chunk */
   uint64_t hash;           /* FNV-1a of inputs + schedule + per-dim order; equal on all ranks */
+  /* The paper's average BW utilisation of the pre-simulated run (PAPER.md:292,
+   * R14): sum_K BW_K busy_K / (sum_K BW_K * makespan) = util_num / util_den,
+   * reduced by their gcd.  util_exact = 1 when the reduced fraction fits in 64
+   * bits (always for the BASELINE configs); 0 = both were shifted right until
+   * they fit (relative error < 2^-60). */
+  uint64_t util_num, util_den;
+  int32_t util_exact;
+  int32_t reserved_info;
 } themis_plan_info_t;
 
 typedef struct themis_plan themis_plan_t;
@@ -259,9 +267,21 @@ themis_status_t themis_trace_fetch(themis_comm_t* comm, uint64_t* out /*[host,ou
  * counter, 3 last CTA's atomic returned, 4 after its fence.acq_rel.sys, 5 unused. */
 themis_status_t themis_trace_fetch_detail(themis_comm_t* comm, uint64_t* out /*[host,out]*/, size_t n);
 
+/* CTA caps proportional to bandwidth (BW emulation by CTA caps, SURVEY a9,
+ * north_star (d)): splits `budget` CTAs over the dims of `topo` as
+ * c_k = max(1, floor(budget * bw_k / sum bw)), then one more CTA to the dims
+ * with the largest remainders budget * bw_k / sum bw - c_k (ties: lower dim
+ * index) while the caps sum below `budget`, or one fewer from the dims with
+ * the smallest remainders among c_k > 1 while they sum above (largest
+ * remainder with a floor of one CTA).  Whenever the roundings
+ * max(1, round(budget * bw_k / sum bw)) sum to `budget` (and no share is a
+ * half-integer), this equals SURVEY a9's c_k = max(1, round(c_tot BW_k / sum BW)).
+ * Exact integer arithmetic.  Errors: INVALID_ARG (budget < ndims, bad topology). */
+themis_status_t themis_default_ctas(const themis_topology_t* topo /*[host]*/, int32_t budget,
+                                    int32_t* ctas_per_dim /*[host,out] ndims*/);
 /* Attach a plan to a comm with per-dimension CTA counts.  ctas_per_dim[k] =
- * CTAs (SMs) of dimension k's group; NULL = proportional to bw_mbps over all
- * SMs.  Capping CTAs per dim emulates heterogeneous per-dimension bandwidth
+ * CTAs (SMs) of dimension k's group; NULL = themis_default_ctas over every
+ * co-resident CTA of the device.  Capping CTAs per dim emulates heterogeneous per-dimension bandwidth
  * on the uniform NVSwitch fabric.  Uploads the per-dim op lists (the plan is
  * immutable afterwards).  Errors: INVALID_ARG (topology differs from the
  * comm's, too many CTAs for co-residency), CUDA. */

@@ -45,7 +45,8 @@ class PlanInfo_t(C.Structure):
                 ("time_scale", C.c_uint64), ("byte_scale", C.c_uint64), ("makespan", C.c_uint64),
                 ("busy", C.c_uint64 * MAX_DIMS), ("idle", C.c_uint64 * MAX_DIMS),
                 ("dim_volume", C.c_uint64 * MAX_DIMS), ("final_load", C.c_uint64 * MAX_DIMS),
-                ("hash", C.c_uint64)]
+                ("hash", C.c_uint64), ("util_num", C.c_uint64), ("util_den", C.c_uint64),
+                ("util_exact", C.c_int32), ("reserved_info", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -81,6 +82,7 @@ SIGNATURES = {
     "themis_comm_enable_trace": (_ST, [_P, C.c_int32]),
     "themis_trace_fetch": (_ST, [_P, _P, C.c_size_t]),
     "themis_trace_fetch_detail": (_ST, [_P, _P, C.c_size_t]),
+    "themis_default_ctas": (_ST, [C.POINTER(Topology_t), C.c_int32, _P]),
     "themis_plan_bind": (_ST, [_P, _P, _P]),
     "themis_plan_bound_ctas": (_ST, [_P, _P]),
     "themis_allreduce": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),

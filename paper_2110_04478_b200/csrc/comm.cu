@@ -107,6 +107,7 @@ struct BindState {
   int32_t ctas[THEMIS_MAX_DIMS] = {};
   int32_t total_ctas = 0;
   bool nvls = false;  // some op runs through the switch (TMA engine only)
+  uint64_t desc_hash = 0;  // of the uploaded op windows / algorithms (mixed into the launch's plan hash)
 };
 }  // namespace themis
 
@@ -338,24 +339,10 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
       n[k] = ctas[k];
       tot += n[k];
     }
-  } else {  // proportional to bandwidth over all SMs, largest remainder, >= 1 each
-    uint64_t sum = 0;
-    for (int k = 0; k < D; ++k) sum += pl->topo.bw_mbps[k];
-    const int budget = std::max(D, c->max_blocks);
-    std::vector<std::pair<double, int>> rem;
-    for (int k = 0; k < D; ++k) {
-      double x = (double)budget * pl->topo.bw_mbps[k] / (double)sum;
-      n[k] = std::max(1, (int)x);
-      tot += n[k];
-      rem.push_back({x - (int)x, k});
-    }
-    std::sort(rem.begin(), rem.end(), [](auto& a, auto& b) { return a.first > b.first || (a.first == b.first && a.second < b.second); });
-    for (size_t i = 0; tot < budget && i < rem.size(); ++i, ++tot) ++n[rem[i].second];
-    while (tot > budget) {  // the >= 1 floor overshot: trim the largest group
-      int kmax = (int)(std::max_element(n, n + D) - n);
-      --n[kmax];
-      --tot;
-    }
+  } else {  // proportional to bandwidth over every co-resident CTA (a9)
+    themis_status_t st = themis_default_ctas(&pl->topo, std::max(D, c->max_blocks), n);
+    if (st != THEMIS_OK) return st;
+    for (int k = 0; k < D; ++k) tot += n[k];
   }
   if (tot > c->max_blocks)
     return fail(THEMIS_ERR_INVALID_ARG, "sum of ctas_per_dim (" + std::to_string(tot) + ") exceeds co-resident CTAs (" +
@@ -460,9 +447,26 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
       }
     }
   }
+  // Everything a peer's CTAs assume about ours: ring step flags are indexed by
+  // absolute CTA, so op windows (min_cta_bytes / window_rotate, settable per
+  // process) and the NVLS rewrite (needs every GPU's multicast mapping) must
+  // be identical on every rank -- hashed here, checked at kernel entry (R22).
+  uint64_t dh = 1469598103934665603ull;
+  auto mix = [&dh](int64_t v) { dh = (dh ^ (uint64_t)v) * 1099511628211ull; };
+  for (const OpDesc& d : ops) {
+    mix(d.width);
+    mix(d.offset);
+    mix(d.ring);
+    mix(d.nvls);
+    mix(d.seq);
+    uint32_t ps;
+    std::memcpy(&ps, &d.pace_scale, 4);
+    mix(ps);
+  }
   free_bind(pl);
   auto* b = new BindState();
   b->comm = c;
+  b->desc_hash = dh;
   cudaError_t e;
   if ((e = cudaMalloc(&b->d_ops, sizeof(OpDesc) * ops.size())) != cudaSuccess ||
       (e = cudaMemcpy(b->d_ops, ops.data(), sizeof(OpDesc) * ops.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -562,10 +566,12 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.trace = c->trace_on ? c->trace : nullptr;
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   // the plan hash covers the inputs, schedule and per-dim order; mix in the
-  // bound CTA caps and the byte count so every rank must launch identically
+  // bound CTA caps, the op descriptors' windows and the byte count so every
+  // rank must launch identically
   {
     uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
     for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
+    h = (h ^ pl->bind->desc_hash) * 1099511628211ull;  // op windows + NVLS rewrite (bind)
     kp.plan_hash = h;
   }
   kp.stages = c->stages;

@@ -1,11 +1,19 @@
 // Device-side building blocks of the Themis executor (sm_100a).
 //
-// Memory-ordering protocol:
-//   producer CTA: data stores -> bar.sync -> fence.sc.sys -> op counter atomic;
-//   the CTA that completes an op publishes epoch-tagged flags with
-//   st.release.sys into the signal pads of the ranks that consume it;
-//   consumers spin with ld.acquire.sys on their own (local) pad, then bar.sync,
-//   then read peer data with L1-bypassing ld.global.cg.
+// Memory-ordering chain of the TMA executor (exec_kernel.cuh), per op:
+//   consumer warps: 16-byte st.global of the op's output -> mbarrier.arrive
+//     (release.cta) on the unit's op_done barrier;
+//   completion warp: mbarrier wait (acquire.cta) -> atom.acq_rel.gpu on the
+//     op's CTA counter; the group's last CTA then runs fence.acq_rel.gpu (every
+//     consumer of the flag on this GPU) or fence.acq_rel.sys (some consumer on
+//     a peer GPU) on every storing lane, and publishes the epoch with
+//     st.relaxed.{gpu,sys} into the consumers' signal pads;
+//   producer warp of a consumer: ld.acquire.sys polls of its own pad ->
+//     fence.proxy.async.global -> cp.async.bulk (TMA) reads of the peer data;
+//   ring slots: consumers' shared-memory reads -> mbarrier.arrive (release) on
+//     empty[s] -> producer's acquire wait -> next TMA write into the slot.
+// Ring-step flags follow the same fence-then-relaxed-store pattern; the entry
+// and exit barriers use st.release.sys / ld.acquire.sys directly.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -223,13 +231,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Relaxed arrive: does not wait for the thread's prior global stores to be
-// performed (a release arrive does, one store round trip per call).  Used to
-// hand a ring slot back to the producer: the slot's shared-memory reads have
-// already completed (their values feed the stores), which is all it orders.
-__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(

@@ -342,16 +342,20 @@ static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + com
 __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { return ((uint32_t)p.stage_bytes / nsrc) & ~15u; }
 
 // Producer (one lane): stream this CTA's tiles of one unit into the ring.
-__device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
+// Returns false if the kernel is aborting (watchdog): every wait for a free
+// ring slot gives up on the abort flag, so a producer whose consumers stopped
+// never spins forever (the CTA then reaches the exit barrier).
+__device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
                                              char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
                                              uint64_t t_op, double& sent) {
   if (mode == U_NVLS || mode == U_NONE) {  // no TMA: a zero-byte token tells the consumers the deps hold
     const int s = ctr % p.stages;
-    dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+    if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) return false;
     dev::mbar_arrive_token(&full[s]);
     ++ctr;
-    return;
+    return true;
   }
+  bool ok = true;
   const int nsrc = unit_nsrc(p, d, mode);
   const uint32_t tile = unit_tile(p, nsrc);
   const float pace = p.pace_ns_per_byte[d.dim] * d.pace_scale;
@@ -359,6 +363,7 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
   const uint64_t pstride = part_stride(p, d.dim);
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+    if (!ok) return;
     const Item m = decode_item(p, d, mode, step, it);
     const char* src[THEMIS_MAX_DIMS > 8 ? THEMIS_MAX_DIMS : 8];
     const int ns = nsrc <= 8 ? nsrc : 8;
@@ -380,7 +385,10 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
             sent += (double)bytes;
           }
           const int s = ctr % p.stages;
-          dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+          if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) {
+            ok = false;
+            return;
+          }
           dev::mbar_expect_tx(&full[s], bytes);
           const char* sj = j < 8 ? src[j]
                                  : data_of(p, unit_src_rank(p, d, mode, m, j)) + m.off +
@@ -399,7 +407,10 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
         sent += (double)bytes * remote;
       }
       const int s = ctr % p.stages;
-      dev::mbar_wait(&empty[s], ((ctr / p.stages) & 1) ^ 1);
+      if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) {
+        ok = false;
+        return;
+      }
       dev::mbar_expect_tx(&full[s], bytes * nsrc);
       char* dst = smem + s * p.stage_bytes;
       for (int j = 0; j < nsrc; ++j) {
@@ -410,6 +421,7 @@ __device__ __forceinline__ void produce_unit(const KParams& p, const OpDesc& d, 
       }
     }
   });
+  return ok;
 }
 
 // Consumers: returns false if the kernel is aborting (watchdog).
@@ -444,7 +456,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         for (; w < w1; w += kCons) dev::mc_st(mc + 16 * w, dev::mc_ld_reduce<Tag>(mc + 16 * w));
       });
     __syncwarp();
-    if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);
+    if (lane == 0) dev::mbar_arrive(&empty[s]);
     ++ctr;
     return true;
   }
@@ -468,7 +480,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
           uint4* dj = reinterpret_cast<uint4*>(base + pos + (uint64_t)peer_member(j, ck) * ps);
           for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dj + w, sm[w]);
           __syncwarp();
-          if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);  // slot reads done; stores ordered by op_done
+          if (lane == 0) dev::mbar_arrive(&empty[s]);  // release: the slot's reads happen-before the producer's next TMA write
         }
       }
       return;
@@ -500,7 +512,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
       }
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive_relaxed(&empty[s]);  // slot reads done; stores ordered by op_done
+      if (lane == 0) dev::mbar_arrive(&empty[s]);  // release: the slot's reads happen-before the producer's next TMA write
     }
   });
   return ok;
@@ -546,13 +558,12 @@ __device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc
   bool local = true;
   for (int v = lane; v < V; v += 32) local &= ring_peer(p, q0 + v, k, +1) / V == p.my_gpu;
   local = __all_sync(0xFFFFFFFFu, local);
-  if (lane == 0) {
-    if (local)
-      dev::fence_acq_rel_gpu();
-    else
-      dev::fence_acq_rel_sys();
-  }
-  __syncwarp();
+  // every storing lane runs the fence (release pattern in its own program
+  // order); it is one warp-wide MEMBAR either way
+  if (local)
+    dev::fence_acq_rel_gpu();
+  else
+    dev::fence_acq_rel_sys();
   for (int v = lane; v < V; v += 32) {
     const int q = q0 + v;
     dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(cur_epoch(), d.seq, step + 1));
@@ -589,14 +600,12 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
       local &= (q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn]) / V == p.my_gpu;
     }
     local = __all_sync(0xFFFFFFFFu, local);
-    if (lane == 0) {
-      if (local)
-        dev::fence_acq_rel_gpu();
-      else
-        dev::fence_acq_rel_sys();
-      if (p.tdetail) p.tdetail[6 * opi + 4] = dev::globaltimer();
-    }
-    __syncwarp();
+    // every storing lane fences (release pattern in its own program order)
+    if (local)
+      dev::fence_acq_rel_gpu();
+    else
+      dev::fence_acq_rel_sys();
+    if (p.tdetail && lane == 0) p.tdetail[6 * opi + 4] = dev::globaltimer();
     for (int t = lane; t < V * pn; t += 32) {
       const int q = q0 + t / pn;
       const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
@@ -706,10 +715,10 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
                 t_op = prev ? prev : now;
               }
             }
-            produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent);
+            if (!produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent)) stop = true;
             if (p.tdetail && li == 0 && u + 1 == nu) p.tdetail[6 * opi + 0] = dev::globaltimer();
           }
-          __syncwarp();
+          stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
         }
         if (stop) break;
       }

@@ -530,6 +530,72 @@ extern "C" themis_status_t themis_plan_info(const themis_plan_t* pl, themis_plan
     info->final_load[k] = (uint64_t)pl->load[k];
   }
   info->hash = pl->hash;
+  // R14 utilisation, exact: sum_K bw_K busy_K / (sum bw * makespan)
+  u128 num = 0, sbw = 0;
+  bool ovf = false;
+  for (int k = 0; k < pl->D; ++k) {
+    const u128 b = pl->topo.bw_mbps[k];
+    sbw += b;
+    if (pl->busy[k] && b > (((u128)-1) - num) / pl->busy[k]) ovf = true;
+    else num += b * pl->busy[k];
+  }
+  u128 den = sbw * pl->makespan;
+  if (pl->makespan && sbw > ((u128)-1) / pl->makespan) ovf = true;
+  if (!ovf && den) {
+    const u128 g = gcd128(num, den);
+    num /= g;
+    den /= g;
+    info->util_exact = 1;
+    while ((num >> 64) || (den >> 64)) {
+      num >>= 1;
+      den >>= 1;
+      info->util_exact = 0;
+    }
+    info->util_num = (uint64_t)num;
+    info->util_den = (uint64_t)den;
+  }
+  return THEMIS_OK;
+}
+
+extern "C" themis_status_t themis_default_ctas(const themis_topology_t* t, int32_t budget, int32_t* n) {
+  if (!t || !n || t->ndims < 1 || t->ndims > THEMIS_MAX_DIMS)
+    return fail(THEMIS_ERR_INVALID_ARG, "bad topology / output");
+  const int D = t->ndims;
+  if (budget < D) return fail(THEMIS_ERR_INVALID_ARG, "budget must be >= ndims (one CTA per dimension at least)");
+  uint64_t sum = 0;
+  for (int k = 0; k < D; ++k) {
+    if (t->bw_mbps[k] == 0) return fail(THEMIS_ERR_INVALID_ARG, "bw == 0");
+    sum += t->bw_mbps[k];
+  }
+  // x_k = budget * bw_k / sum;  n_k = max(1, floor(x_k));  r_k = (x_k - n_k) * sum
+  // (negative for dims raised to the 1-CTA floor).  Largest r_k gains one CTA
+  // while the caps sum below budget; the smallest r_k among n_k > 1 loses one
+  // while they sum above (ties: lower dim index).  Exact integers.
+  using i128 = __int128;
+  i128 r[THEMIS_MAX_DIMS];
+  int tot = 0;
+  for (int k = 0; k < D; ++k) {
+    const i128 x = (i128)budget * t->bw_mbps[k];
+    n[k] = std::max<int32_t>(1, (int32_t)(x / (i128)sum));
+    r[k] = x - (i128)n[k] * (i128)sum;
+    tot += n[k];
+  }
+  while (tot < budget) {
+    int best = 0;
+    for (int k = 1; k < D; ++k)
+      if (r[k] > r[best]) best = k;
+    ++n[best];
+    r[best] -= (i128)sum;
+    ++tot;
+  }
+  while (tot > budget) {
+    int best = -1;
+    for (int k = 0; k < D; ++k)
+      if (n[k] > 1 && (best < 0 || r[k] < r[best])) best = k;
+    --n[best];
+    r[best] += (i128)sum;
+    --tot;
+  }
   return THEMIS_OK;
 }
 

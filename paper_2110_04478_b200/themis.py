@@ -128,6 +128,7 @@ class Plan:
             "n_greedy": i.n_greedy, "time_scale": i.time_scale, "byte_scale": i.byte_scale,
             "makespan": i.makespan, "busy": list(i.busy[:D]), "idle": list(i.idle[:D]),
             "dim_volume": list(i.dim_volume[:D]), "final_load": list(i.final_load[:D]), "hash": i.hash,
+            "util_num": i.util_num, "util_den": i.util_den, "util_exact": bool(i.util_exact),
         }
         self.n_chunks = i.n_chunks          # the planner's choice when n_chunks = 0 (auto)
 
@@ -183,10 +184,9 @@ class Plan:
 
     def utilization(self) -> Fraction:
         """The paper's average BW utilisation of the pre-simulated run,
-        sum_K BW_K busy_K / (sum BW * makespan) (R14), exact."""
-        bw = [int(b) for b in self.topo.bw_mbps]
-        busy = self.info["busy"]
-        return Fraction(sum(b * t for b, t in zip(bw, busy)), sum(bw) * self.info["makespan"])
+        sum_K BW_K busy_K / (sum BW * makespan) (R14), as the
+        library computes it (themis_plan_info_t.util_num / util_den)."""
+        return Fraction(self.info["util_num"], self.info["util_den"])
 
     def makespan_ns(self) -> Fraction:
         return Fraction(self.info["makespan"], self.info["time_scale"])
@@ -506,19 +506,12 @@ def run(coll: int, comm: Comm, plan: Plan, count: int, dtype: str, stream=None) 
 
 
 def default_ctas(bw: Sequence[int], total: int) -> list:
-    """CTA caps per dimension proportional to bandwidth (largest remainder,
-    >= 1 each) — the bandwidth-emulation knob (north_star (d))."""
-    s = sum(bw)
-    raw = [total * b / s for b in bw]
-    n = [max(1, int(x)) for x in raw]
-    order = sorted(range(len(bw)), key=lambda k: (-(raw[k] - int(raw[k])), k))
-    i = 0
-    while sum(n) < total:
-        n[order[i % len(bw)]] += 1
-        i += 1
-    while sum(n) > total:
-        n[n.index(max(n))] -= 1
-    return n
+    """CTA caps per dimension proportional to bandwidth — the bandwidth-
+    emulation knob (north_star (d)): themis_default_ctas."""
+    t = Topology(tuple([2] * len(bw)), tuple(int(b) for b in bw)).to_c()
+    out = (C.c_int32 * MAX_DIMS)()
+    check(lib().themis_default_ctas(C.byref(t), int(total), out))
+    return list(out[:len(bw)])
 
 
 def launches_per_call() -> int:

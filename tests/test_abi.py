@@ -42,6 +42,26 @@ def test_heap_layout():
     assert stride2 % 65536 == 0 and heap2 == sig2 + stride2
 
 
+def test_default_ctas_is_the_a9_formula():
+    """themis_default_ctas == SURVEY a9's c_k = max(1, round(c_tot BW_k / sum BW))
+    whenever those roundings already sum to c_tot; always sums to c_tot, >= 1."""
+    import random
+    from fractions import Fraction
+    rng = random.Random(7)
+    agree = 0
+    for _ in range(2000):
+        D = rng.randint(1, 8)
+        bw = [rng.choice([1, 2, 3, 4, 7, 50, 200, 1000, rng.randint(1, 10**6)]) for _ in range(D)]
+        total = rng.randint(D, 400)
+        got = th.default_ctas(bw, total)
+        assert sum(got) == total and min(got) >= 1, (bw, total, got)
+        want = [max(1, round(Fraction(total * b, sum(bw)))) for b in bw]   # half-to-even ties are remainder ties
+        if sum(want) == total and all(Fraction(total * b, sum(bw)) % 1 != Fraction(1, 2) for b in bw):
+            assert got == want, (bw, total, got, want)
+            agree += 1
+    assert agree > 500
+
+
 def test_default_ctas():
     assert th.default_ctas((4, 2, 1), 28) == [16, 8, 4]
     assert th.default_ctas((1, 1, 1), 148) == [50, 49, 49]
