@@ -30,7 +30,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "All-Reduce bus GB/s vs 900 GB/s NVLink at 2/4/8 B200, Themis vs baseline order"
 SIZES = (2, 2, 2)
-NVLINK_PEAK = 770.0       # measured peer-copy GB/s per direction (B200_PROFILING.md; 900 nominal)
+NVLINK_PEAK = 770.0       # measured peer-copy GB/s per direction (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0    # nominal per direction per GPU (the metric's denominator)
 
 
 def logical_layout(sizes, n_gpus):
@@ -232,6 +233,14 @@ def run_themis(a):
     busbw = lambda t: 2 * S * (P - 1) / P / t / 1e9
 
     main = make(th.THEMIS, ratio)
+    # planner cost (SURVEY.md:557): the C++ planner (themis_plan: Algorithm 1 +
+    # pre-simulation) for this exact request, median of 21 calls
+    pts = []
+    for _ in range(21):
+        t0 = time.perf_counter()
+        th.Plan(th.Topology(SIZES, ratio, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF).close()
+        pts.append(time.perf_counter() - t0)
+    planner_cpp_us = round(statistics.median(pts) * 1e6, 1)
     clocks = ClockSampler(local)
     with clocks:
         t_main, t_best = timed(main, a.steps, a.warmup)
@@ -427,7 +436,8 @@ def run_themis(a):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
     else:
         roof = {"bound": "nvlink", "achieved": round(nvl_ach, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
-                "frac": round(nvl_ach / NVLINK_PEAK, 4), "traffic": None,
+                "frac": round(nvl_ach / NVLINK_PEAK, 4), "frac_of_900_nominal": round(nvl_ach / NVLINK_NOMINAL, 4),
+                "traffic": None,
                 "algorithmic_bytes_per_launch": nvl_bytes,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"}
     roof["kernel"] = "themis_exec_kernel<F32Tag,true> (TMA engine)"
@@ -444,6 +454,19 @@ def run_themis(a):
     if world == 1 and not a.no_cpu:
         cpu = cpu_baseline(a.cpu_mib, a.chunks, ratio, reps=8)   # ~10 s of CPU work
 
+    # Themis vs baseline under emulated heterogeneous BW (the metric's second
+    # half): the paced rows carry the paper's utilisation; the headline ratio
+    # 4:2:1 is the Just-Enough control (equal by construction)
+    tvb = {}
+    for key, row in compare.items():
+        ent = {"measured_speedup": row["measured_speedup"], "model_speedup": row["model_speedup"],
+               "themis_bus_gbs": row["themis"]["bus_gbs"], "baseline_bus_gbs": row["baseline"]["bus_gbs"]}
+        if "sum_bw_gbs" in row:
+            ent.update(sum_bw_gbs=row["sum_bw_gbs"], themis_util=row["themis"]["util"],
+                       baseline_util=row["baseline"]["util"],
+                       frac_of_model_speedup=round(row["measured_speedup"] / row["model_speedup"], 3))
+        tvb[key] = ent
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(busbw(t_main), 2), "unit": "GB/s", "n_gpus": world,
@@ -457,6 +480,14 @@ def run_themis(a):
                         f"rank, {a.chunks} chunks, emulated BW {a.ratio}"),
                        "topology": "x".join(map(str, SIZES)), "bytes_per_rank": S, "chunks": a.chunks,
                        "bw_ratio": a.ratio, "policy": "themis+scf", "ranks_per_gpu": V,
+                       "ratio_note": ("4:2:1 on 2x2x2 is the paper's Just-Enough ratio (PAPER.md:703-705): Algorithm 1 "
+                                      "keeps all 64 chunks on the baseline order, so Themis == baseline here by "
+                                      "construction; the Themis effect is in themis_vs_baseline (over-provisioned "
+                                      "1:1:1 / 2:2:1, paced emulation)") if a.ratio == "4:2:1" and SIZES == (2, 2, 2)
+                                     else None,
+                       "emulation": ("CTA caps only (value is the unthrottled kernel: with every dim's group "
+                                     "sharing one HBM / NVLink fabric the caps do not bind; paced rows in "
+                                     "themis_vs_baseline emulate BW_K exactly)"),
                        "ops_in_flight_per_dim": max(1, a.concurrency),
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
                        "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages, "tma_stage_kib": stage_kb,
@@ -470,6 +501,8 @@ def run_themis(a):
                        "l2": "inputs refreshed from a pristine copy before every step (>= 1 GiB per GPU written, "
                              "> 126 MB L2); inputs larger than L2"},
             "clocks": clocks.summary(), "gpu_launches": launches, "roofline": roof, "e2e": e2e,
+            "themis_vs_baseline": tvb, "planner": {"cpp_us": planner_cpp_us,
+                                                   "oracle_ms": cpu.get("planner_oracle_ms") if cpu else None},
             "compare": compare, "per_dim_emulation": per_dim, "nccl_context": nccl, "cpu_baseline": cpu,
         }
         emit(out)
@@ -494,7 +527,14 @@ def cpu_baseline(mib, chunks, ratio, reps=1):
     for _ in range(reps):
         O.run_schedule(xs, sched, "f32")
     dt = (time.perf_counter() - t0) / reps
+    # the oracle planner (Fractions: Algorithm 1 + the event pre-simulation) on
+    # the full-size request, for the planner-time comparison (SURVEY.md:557)
+    from oracle import engine as E_
+    t1 = time.perf_counter()
+    E_.simulate(S_.schedule_collective(t, S_.AR, 1 << 30, chunks, S_.THEMIS), E_.SCF)
+    plan_ms = (time.perf_counter() - t1) * 1e3
     return {"value": round(2 * N * 4 * (P - 1) / P / dt / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "planner_oracle_ms": round(plan_ms, 2),
             "host_cores_available": len(os.sched_getaffinity(0)), "kind": "oracle",
             "sample": f"{'x'.join(map(str, SIZES))} Themis All-Reduce, {mib} MiB fp32 per rank x {P} simulated "
                       f"ranks, {chunks} chunks, numpy single-threaded, {reps} rep(s), {dt:.2f} s per All-Reduce"}

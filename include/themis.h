@@ -286,6 +286,13 @@ themis_status_t themis_default_ctas(const themis_topology_t* topo /*[host]*/, in
  * immutable afterwards).  Errors: INVALID_ARG (topology differs from the
  * comm's, too many CTAs for co-residency), CUDA. */
 themis_status_t themis_plan_bind(themis_plan_t* plan, themis_comm_t* comm, const int32_t* ctas_per_dim /*[host] D or NULL*/);
+/* The 64-bit hash a collective launched with this bound plan, count and dtype
+ * announces at its entry barrier (plan hash + count + dtype + CTA caps + op
+ * windows / NVLS rewrite); ranks whose hashes differ latch PLAN_MISMATCH
+ * (R22).  For diagnosing mismatches and for fault-injection tests.
+ * Errors: PLAN_MISMATCH if the plan is not bound. */
+themis_status_t themis_plan_launch_hash(const themis_plan_t* plan, uint64_t count, int32_t dtype,
+                                        uint64_t* hash /*[host,out]*/);
 /* CTAs per dimension group a bound plan launches with ([host, out] D entries).
  * Errors: PLAN_MISMATCH if the plan is not bound. */
 themis_status_t themis_plan_bound_ctas(const themis_plan_t* plan, int32_t* ctas_per_dim /*[host,out]*/);

@@ -523,6 +523,22 @@ static themis_status_t check_call(int coll, void* buf, uint64_t count, int32_t d
   return THEMIS_OK;
 }
 
+// The plan hash covers the inputs, schedule and per-dim order; mix in the
+// bound CTA caps, the op descriptors' windows and the byte count so every rank
+// must launch identically (checked at kernel entry, R22).
+static uint64_t launch_hash(const themis_plan_t* pl, uint64_t count, int32_t dtype) {
+  uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
+  for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
+  return (h ^ pl->bind->desc_hash) * 1099511628211ull;  // op windows + NVLS rewrite (bind)
+}
+
+extern "C" themis_status_t themis_plan_launch_hash(const themis_plan_t* pl, uint64_t count, int32_t dtype,
+                                                   uint64_t* out) {
+  if (!pl || !pl->bind || !out) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan not bound / null output");
+  *out = launch_hash(pl, count, dtype);
+  return THEMIS_OK;
+}
+
 static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype, const themis_plan_t* pl,
                               void* stream, uint32_t host_seq = 0) {
   int esz = 0;
@@ -565,15 +581,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.timeout_ns = c->timeout_ns;
   kp.trace = c->trace_on ? c->trace : nullptr;
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
-  // the plan hash covers the inputs, schedule and per-dim order; mix in the
-  // bound CTA caps, the op descriptors' windows and the byte count so every
-  // rank must launch identically
-  {
-    uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
-    for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
-    h = (h ^ pl->bind->desc_hash) * 1099511628211ull;  // op windows + NVLS rewrite (bind)
-    kp.plan_hash = h;
-  }
+  kp.plan_hash = launch_hash(pl, count, dtype);
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;
   kp.ag_rr = c->ag_rr;

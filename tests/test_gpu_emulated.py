@@ -327,6 +327,56 @@ def test_watchdog_on_missing_peer():
     lib().themis_heap_free(h1)
 
 
+def test_watchdog_mid_collective():
+    """a peer that passes the entry barrier but never publishes a
+    stage's ready flags must time out *after* other dimension groups started
+    streaming (producers blocked on ring slots give up on the abort flag) and
+    the launch must return with THEMIS_ERR_TIMEOUT latched, not hang.
+    W = 2, P = 4 (2x2): GPU 0 is real (ranks 0, 1; dim1 local), "GPU 1" is a
+    silent heap on the same device whose ranks 2, 3 are faked as having
+    entered (entry epoch + launch hash written into our pads)."""
+    import ctypes as C
+    import time
+    from paper_2110_04478_b200._lib import MAX_GPUS, check, lib
+    topo = th.Topology((2, 2), (1, 1))
+    P, C_ = 4, 16
+    N = P * C_ * (1 << 18)                                  # 64 MiB fp32 per rank: dim1 streams for ms
+    sig, stride, hb = th.heap_layout(P, 2, N * 4)
+    h0, h1 = C.c_void_p(), C.c_void_p()
+    check(lib().themis_heap_alloc(hb, C.byref(h0)))
+    check(lib().themis_heap_alloc(hb, C.byref(h1)))
+    heaps = (C.c_void_p * MAX_GPUS)(h0.value, h1.value)
+    comm = C.c_void_p()
+    tc = topo.to_c()
+    check(lib().themis_comm_create(0, 2, C.byref(tc), heaps, hb, stride, C.byref(comm)))
+    check(lib().themis_comm_set_timeout(comm, int(0.5e9)))
+    plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_, th.THEMIS)
+    check(lib().themis_plan_bind(plan.h, comm, None))
+    hsh = C.c_uint64()
+    check(lib().themis_plan_launch_hash(plan.h, N, 0, C.byref(hsh)))
+    # signal pad of local rank v: [entry u32 P][exit u32 P][ready u32 P x kMaxOps][ring u64 P x 8 x 160][hash u64 P]
+    k_max_ops, ring_off = 1024 * 2 * 8, 4 * (2 * P + P * 1024 * 2 * 8)
+    hash_off = ring_off + 8 * P * 8 * 160
+    for v in range(2):
+        pad = torch.as_tensor(th._CAI(h0.value + v * sig, sig // 4, "<i4"), device="cuda")
+        s32 = lambda x: x - (1 << 32) if x >= (1 << 31) else x
+        for src in (2, 3):                                  # the fake GPU's ranks entered epoch 1 ...
+            pad[src] = 1
+            pad[hash_off // 4 + 2 * src] = s32(hsh.value & 0xFFFFFFFF)    # ... with the identical plan
+            pad[hash_off // 4 + 2 * src + 1] = s32(hsh.value >> 32)
+    assert k_max_ops == 16384
+    torch.cuda.synchronize()
+    t0 = time.time()
+    check(lib().themis_allreduce(h0.value + 2 * sig, N, 0, plan.h, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 10
+    assert lib().themis_comm_status(comm) == 8
+    plan.close()
+    lib().themis_comm_free(comm)
+    lib().themis_heap_free(h0)
+    lib().themis_heap_free(h1)
+
+
 def test_trace_follows_enforced_order():
     topo = th.Topology((2, 2, 2), (1, 1, 1))
     C_ = 8
