@@ -241,6 +241,18 @@ themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t byte
  * small op occupies (and synchronises) only the CTAs it needs.  Takes effect at
  * the next themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rotate);
+/* Runtime intra-dimension order (DESIGN R28).  lookahead = 1
+ * (default, env THEMIS_LOOKAHEAD): every dimension group runs its ops in the
+ * pre-simulated enforced order.  L in 2..32: on dims that
+ * run the direct algorithm (no ring steps, no NVLS op), each CTA's producer
+ * takes, among the next L not-yet-taken ops of the enforced list, the first
+ * whose dependencies already hold (the enforced order stays the priority;
+ * readiness decides), so a late op no longer blocks ready ones behind it.
+ * Ranks may then run a dimension's ops in different orders, which the
+ * pull-based executor tolerates (every op reads only its peers' finished
+ * (c, s-1) data; R28).  Takes effect at the next collective.
+ * Errors: INVALID_ARG. */
+themis_status_t themis_comm_set_lookahead(themis_comm_t* comm, int32_t lookahead);
 /* NVLS (in-switch reduction): mc_heap [device] = the
  * multicast (NVSwitch) mapping of this GPU's heap, at the same offsets, bound
  * on all W GPUs (e.g. torch symmetric memory's multicast pointer); NULL = off.

@@ -86,6 +86,7 @@ struct themis_comm {
   int ag_rr = 0;                  // direct-AG tile shape (env THEMIS_AG_RR, experiment)
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
+  int lookahead = 1;           // runtime intra-dim order window (themis_comm_set_lookahead); 1 = static
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -107,6 +108,7 @@ struct BindState {
   int32_t ctas[THEMIS_MAX_DIMS] = {};
   int32_t total_ctas = 0;
   bool nvls = false;  // some op runs through the switch (TMA engine only)
+  uint32_t dyn_mask = 0;  // dims whose ops may take the runtime order (direct algorithm, no NVLS op)
   uint64_t desc_hash = 0;  // of the uploaded op windows / algorithms (mixed into the launch's plan hash)
 };
 }  // namespace themis
@@ -215,6 +217,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     c->stages = std::max(1, std::min(std::min(kStages, kStages * kStageBytes / c->stage_bytes), atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   if (const char* env = getenv("THEMIS_WINDOW_ROTATE")) c->window_rotate = atoi(env) != 0;
+  if (const char* env = getenv("THEMIS_LOOKAHEAD")) c->lookahead = std::max(1, std::min(kMaxLookahead, atoi(env)));
   c->max_blocks = nb * c->num_sms;
   *out = c;
   return THEMIS_OK;
@@ -263,6 +266,11 @@ extern "C" themis_status_t themis_comm_set_multicast(themis_comm_t* c, void* mc_
 extern "C" themis_status_t themis_comm_set_window_rotation(themis_comm_t* c, int32_t rotate) {
   if (!c || rotate < 0 || rotate > 1) return fail(THEMIS_ERR_INVALID_ARG, "rotate must be 0 or 1");
   c->window_rotate = rotate;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_lookahead(themis_comm_t* c, int32_t lookahead) {
+  if (!c || lookahead < 1 || lookahead > kMaxLookahead) return fail(THEMIS_ERR_INVALID_ARG, "lookahead must be 1..32");
+  c->lookahead = lookahead;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* c, uint64_t bytes) {
@@ -483,6 +491,9 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   }
   b->total_ctas = tot;
   b->nvls = any_nvls;
+  b->dyn_mask = (1u << D) - 1;
+  for (const OpDesc& d : ops)
+    if (d.ring || d.nvls) b->dyn_mask &= ~(1u << d.dim);
   pl->bind = b;
   c->bound.push_back(pl);
   return THEMIS_OK;
@@ -582,6 +593,8 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.trace = c->trace_on ? c->trace : nullptr;
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   kp.plan_hash = launch_hash(pl, count, dtype);
+  kp.lookahead = c->lookahead;
+  kp.dyn_mask = pl->bind->dyn_mask;
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;
   kp.ag_rr = c->ag_rr;

@@ -64,6 +64,8 @@ struct KParams {
   uint64_t* trace;          // [C*NS*2] or null
   uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
+  int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
+  uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
@@ -335,8 +337,10 @@ __device__ void run_op_ldg(const KParams& p, const OpDesc& d, int gi, int gn) {
 constexpr int kStages = 6;
 constexpr int kStageBytes = 32 * 1024;
 constexpr int kConsumerWarps = 8;
-constexpr int kOpRing = 16;  // units the consumers may run ahead of the completion warp
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * (kStages + kOpRing) * 8;
+constexpr int kOpRing = 16;  // units the producer / consumers may run ahead of the completion warp
+// ring [stages x stage bytes] | full, empty [kStages] | op_done, op_free, q_full [kOpRing] | unit queue int [kOpRing]
+constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 3 * kOpRing) * 8 + kOpRing * 4;
+constexpr int kMaxLookahead = 32;
 static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + completion warp");
 
 __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { return ((uint32_t)p.stage_bytes / nsrc) & ~15u; }
@@ -535,6 +539,21 @@ __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d
   return __all_sync(0xFFFFFFFFu, ok);
 }
 
+// One warp, non-blocking: have the local ranks' and their dim-k peers' (c, s-1)
+// (or the host copies of chunk c) completed?  One acquire load per flag.
+__device__ __forceinline__ bool deps_ready_warp(const KParams& p, const OpDesc& d, int opi) {
+  if (d.stage == 0 && !p.host_seq) return true;
+  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
+  bool ok = true;
+  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
+    const int q = q0 + t / pk;
+    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+    ok &= d.stage > 0 ? dev::ld_acquire_sys(ready_slot(p, q, src, opi - 1)) >= cur_epoch()
+                      : dev::ld_acquire_sys(h2d_slot(p, src / V, d.chunk)) >= p.host_seq;
+  }
+  return __all_sync(0xFFFFFFFFu, ok);
+}
+
 __device__ __forceinline__ unsigned long long ring_flag_value(uint32_t epoch, int seq, int steps_done) {
   return ((unsigned long long)epoch << 32) | ((unsigned long long)seq << 8) | (unsigned long long)steps_done;
 }
@@ -649,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     for (int s = 0; s < kOpRing; ++s) {
       dev::mbar_init(&op_done[s], kConsumerWarps);
       dev::mbar_init(&op_free[s], 1);
+      dev::mbar_init(&op_free[s] + kOpRing, 1);  // q_full[s]: the producer announced unit s
     }
     dev::fence_mbar_init();
   }
@@ -678,27 +698,107 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
   const int* list = p.dim_ops + (uint64_t)g * p.C * p.NS;
   const int nops = ok ? p.dim_ops_n[g] : 0;
   if constexpr (kTma) {
-    // Decoupled: the producer waits for a unit's dependencies and streams its
-    // tiles, then moves on while the consumers finish; the completion warp
-    // counts and publishes, so no sys fence ever stalls the tile stream.
-    uint32_t ctr = 0;  // ring position (identical sequence in producer and consumers)
+    // Decoupled: the producer picks the next op, waits for its dependencies,
+    // streams its tiles and moves on while the consumers finish; the
+    // completion warp counts and publishes, so no sys fence ever stalls the
+    // tile stream.  The producer announces every unit it takes (op, ring step)
+    // in a shared-memory queue that the consumers and the completion warp
+    // follow, so the order is the producer's alone:
+    //   static (default; ring dims, NVLS): the enforced order;
+    //   runtime (lookahead L > 1, direct dims): the first op among the next L
+    //   not-yet-taken ops of the enforced list whose dependencies already
+    //   hold -- the pre-simulated order is the priority, readiness decides
+    //   (SURVEY NEXT-3, R28).  Pull-based ops only read peers' finished
+    //   (c, s-1) data, so ranks need not agree on the order (R28).
+    uint32_t ctr = 0;  // tile ring position (identical sequence in producer and consumers)
+    uint64_t* q_full = op_free + kOpRing;
+    int* s_q = reinterpret_cast<int*>(q_full + kOpRing);
+    // this CTA's units: sum of ring steps over the ops it is a member of
+    int my_units = 0;
+    if (warp > 0) {
+      for (int i = lane; i < nops; i += 32) {
+        const OpDesc& d = p.ops[list[i]];
+        int li, wn;
+        if (op_member(d, gi, gn, li, wn)) my_units += d.ring ? p.size[d.dim] - 1 : 1;
+      }
+      for (int o = 16; o; o >>= 1) my_units += __shfl_xor_sync(0xFFFFFFFFu, my_units, o);
+    }
     if (warp == 0) {
-      for (int i = 0; i < nops; ++i) {
-        const int opi = list[i];
+      const bool dyn = p.lookahead > 1 && (p.dyn_mask >> g & 1u);
+      const int LA = dyn ? (p.lookahead < kMaxLookahead ? p.lookahead : kMaxLookahead) : 1;
+      int head = 0;           // first list position not yet taken
+      uint32_t taken = 0;     // bit j: list[head + j] taken
+      uint32_t nq = 0;        // units announced
+      bool stop = false;
+      uint64_t t_wait = 0;
+      while (!stop) {
+        while (head < nops) {  // drop taken / foreign ops at the head
+          int li, wn;
+          if (!(taken & 1u) && op_member(p.ops[list[head]], gi, gn, li, wn)) break;
+          taken >>= 1;
+          ++head;
+        }
+        if (head >= nops) break;
+        int pick = 0;
+        if (dyn) {
+          pick = -1;
+          for (int j = 0; j < LA && head + j < nops && pick < 0; ++j) {
+            if (taken >> j & 1u) continue;
+            const int opi = list[head + j];
+            const OpDesc& d = p.ops[opi];
+            int li, wn;
+            if (!op_member(d, gi, gn, li, wn)) continue;
+            if (!unit_has_work(p, d, unit_mode_tma(d), li, wn) || deps_ready_warp(p, d, opi)) pick = j;
+          }
+          if (pick < 0) {  // nothing ready yet: watchdog (decided on lane 0, warp-uniform), then scan again
+            int give_up = 0;
+            if (lane == 0) {
+              const uint64_t now = dev::globaltimer();
+              if (!t_wait) t_wait = now;
+              if (*(volatile uint32_t*)p.abort_flag) {
+                give_up = 1;
+              } else if (now - t_wait > p.timeout_ns) {
+                atomicExch(p.abort_flag, 1u);
+                *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_TIMEOUT | ((uint32_t)list[head] << 8);
+                __threadfence_system();
+                give_up = 1;
+              }
+            }
+            if (__shfl_sync(0xFFFFFFFFu, give_up, 0)) break;
+            continue;
+          }
+          t_wait = 0;
+        }
+        taken |= 1u << pick;
+        const int opi = list[head + pick];
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
-        if (!op_member(d, gi, gn, li, wn)) continue;          // op runs on other CTAs of the group
-        if (!unit_has_work(p, d, mode, li, wn)) continue;     // nothing to wait for or move
+        op_member(d, gi, gn, li, wn);
+        const bool work = unit_has_work(p, d, mode, li, wn);
         uint64_t t_op = 0;
         double sent = 0.0;
-        bool stop = false;
-        for (int u = 0; u < nu && !stop; ++u) {
+        for (int u = 0; u < nu && !stop; ++u, ++nq) {
+          const int slot = nq % kOpRing;
+          bool w = true;
+          if (lane == 0) {  // announce the unit once the followers released the queue slot
+            w = dev::mbar_wait_or(&op_free[slot], ((nq / kOpRing) & 1) ^ 1, p.abort_flag);
+            if (w) {
+              s_q[slot] = opi * 64 + u;
+              dev::mbar_arrive(&q_full[slot]);
+            }
+          }
+          if (!__shfl_sync(0xFFFFFFFFu, w, 0)) {
+            stop = true;
+            break;
+          }
+          if (!work) continue;  // nothing to wait for or move: the followers just count it
           // ring step flags are per absolute CTA index gi: each CTA's slot then
           // sees its ops in order (monotone), and CTA gi of the left neighbour
           // has the same window index li for this op (identical windows).
-          if (u == 0 ? ((d.stage > 0 || p.host_seq) && !wait_deps_warp(p, d, opi)) : !wait_ring_warp(p, d, u, gi)) {
+          if (u == 0 ? (!dyn && (d.stage > 0 || p.host_seq) && !wait_deps_warp(p, d, opi))
+                     : !wait_ring_warp(p, d, u, gi)) {
             stop = true;
             break;
           }
@@ -720,68 +820,53 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           }
           stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
         }
-        if (stop) break;
       }
     } else if (warp <= kConsumerWarps) {
-      // consumers: per unit, every consumer warp arrives on op_done[slot]
-      // (mbarrier arrive = release.cta of its stores) after the completion
-      // warp has freed that slot (ring of kOpRing units).
-      int n = 0;
-      bool run = true;
-      for (int i = 0; i < nops && run; ++i) {
-        const int opi = list[i];
+      // consumers: per announced unit, every consumer warp arrives on
+      // op_done[slot] (mbarrier arrive = release.cta of its stores) after the
+      // completion warp has freed that slot (ring of kOpRing units).
+      for (int n = 0; n < my_units; ++n) {
+        const int slot = n % kOpRing;
+        if (!dev::mbar_wait_or(&q_full[slot], (n / kOpRing) & 1, p.abort_flag)) break;
+        const int e = s_q[slot], opi = e >> 6, u = e & 63;
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
-        if (!op_member(d, gi, gn, li, wn)) continue;
-        for (int u = 0; u < nu; ++u, ++n) {
-          if (!consume_unit<Tag>(p, d, mode, u, li, wn, smem, full, empty, ctr)) {
-            run = false;
-            break;
-          }
-          __syncwarp();
-          bool w = true;
-          if (lane == 0) {
-            if (p.tdetail && li == 0 && warp == 1 && u + 1 == nu) p.tdetail[6 * opi + 1] = dev::globaltimer();
-            const int slot = n % kOpRing;
-            w = dev::mbar_wait_or(&op_free[slot], ((n / kOpRing) & 1) ^ 1, p.abort_flag);
-            if (w) dev::mbar_arrive(&op_done[slot]);
-          }
-          if (!__shfl_sync(0xFFFFFFFFu, w, 0)) {
-            run = false;
-            break;
-          }
+        op_member(d, gi, gn, li, wn);
+        if (!consume_unit<Tag>(p, d, mode, u, li, wn, smem, full, empty, ctr)) break;
+        __syncwarp();
+        bool w = true;
+        if (lane == 0) {
+          if (p.tdetail && li == 0 && warp == 1 && u + 1 == nu) p.tdetail[6 * opi + 1] = dev::globaltimer();
+          w = dev::mbar_wait_or(&op_free[slot], ((n / kOpRing) & 1) ^ 1, p.abort_flag);
+          if (w) dev::mbar_arrive(&op_done[slot]);
         }
+        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
       }
     } else {
       // completion warp: ring steps publish per-CTA step flags; the last unit
       // of an op counts group-wide and publishes the op's ready flags.
-      int n = 0;
-      bool run = true;
-      for (int i = 0; i < nops && run; ++i) {
-        const int opi = list[i];
+      for (int n = 0; n < my_units; ++n) {
+        const int slot = n % kOpRing;
+        bool w = true;
+        if (lane == 0)
+          w = dev::mbar_wait_or(&q_full[slot], (n / kOpRing) & 1, p.abort_flag) &&
+              dev::mbar_wait_or(&op_done[slot], (n / kOpRing) & 1, p.abort_flag);
+        if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
+        const int e = s_q[slot], opi = e >> 6, u = e & 63;
         const OpDesc& d = p.ops[opi];
         const int mode = unit_mode_tma(d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
-        if (!op_member(d, gi, gn, li, wn)) continue;
-        const bool work = unit_has_work(p, d, mode, li, wn);
-        for (int u = 0; u < nu; ++u, ++n) {
-          const int slot = n % kOpRing;
-          bool w = true;
-          if (lane == 0) w = dev::mbar_wait_or(&op_done[slot], (n / kOpRing) & 1, p.abort_flag);
-          if (!__shfl_sync(0xFFFFFFFFu, w, 0)) {
-            run = false;
-            break;
-          }
-          if (u + 1 < nu) {
-            if (work) publish_ring_warp(p, d, u, gi);
-          } else {
-            complete_op_warp(p, d, opi, wn);
-          }
-          if (lane == 0) dev::mbar_arrive(&op_free[slot]);
+        op_member(d, gi, gn, li, wn);
+        if (u + 1 < nu) {
+          if (unit_has_work(p, d, mode, li, wn)) publish_ring_warp(p, d, u, gi);
+        } else {
+          complete_op_warp(p, d, opi, wn);
         }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&op_free[slot]);
       }
     }
   } else {

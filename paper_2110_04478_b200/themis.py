@@ -332,6 +332,11 @@ class Comm:
         """Op windows: consecutive windows (True) or every narrow op from CTA 0."""
         check(lib().themis_comm_set_window_rotation(self.h, int(rotate)))
 
+    def set_lookahead(self, lookahead: int) -> None:
+        """Runtime intra-dim order: 1 = the enforced pre-simulated order;
+        L > 1 = first ready op among the next L of it (direct dims, R28)."""
+        check(lib().themis_comm_set_lookahead(self.h, int(lookahead)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib().themis_comm_set_timeout(self.h, int(seconds * 1e9)))
 

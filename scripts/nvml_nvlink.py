@@ -39,26 +39,46 @@ def n_links(handle) -> int:
     return n
 
 
-def read(index: int):
-    """(tx_bytes, rx_bytes, links) summed over the GPU's active links."""
-    _init()
-    h = nv.nvmlDeviceGetHandleByIndex(index)
-    links = n_links(h)
+# (tx field, rx field, unit bytes): Blackwell exposes the per-link byte
+# counters (COUNT_XMIT/RCV_BYTES); older parts the KiB throughput counters
+FIELD_SETS = [("NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 1),
+              ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX", 1024)]
+_WORKING = {}
+
+
+def _try(h, links, fs):
+    tx_f, rx_f, unit = getattr(nv, fs[0]), getattr(nv, fs[1]), fs[2]
     fields = []
     for link in range(links):
-        fields.append((nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link))
-        fields.append((nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link))
+        fields.append((tx_f, link))
+        fields.append((rx_f, link))
     vals = nv.nvmlDeviceGetFieldValues(h, fields)
     tx = rx = 0
     for i, v in enumerate(vals):
         if v.nvmlReturn != nv.NVML_SUCCESS:
-            raise RuntimeError(f"NVML field {fields[i]} returned {v.nvmlReturn}")
+            raise RuntimeError(f"{fs[i % 2]} link {i // 2}: NVML return {v.nvmlReturn}")
         x = int(v.value.ullVal)
         if i % 2 == 0:
             tx += x
         else:
             rx += x
-    return tx * 1024, rx * 1024, links      # counters are in KiB
+    return tx * unit, rx * unit
+
+
+def read(index: int):
+    """(tx_bytes, rx_bytes, links, field set) summed over the GPU's active links."""
+    _init()
+    h = nv.nvmlDeviceGetHandleByIndex(index)
+    links = n_links(h)
+    errs = []
+    for fs in ([_WORKING[index]] if index in _WORKING else FIELD_SETS):
+        try:
+            tx, rx = _try(h, links, fs)
+            _WORKING[index] = fs
+            return tx, rx, links, fs[0]
+        except Exception as e:       # try the next field set; report all if none works
+            errs.append(str(e))
+    raise RuntimeError("; ".join(errs))
 
 
 class NvlinkCounters:
@@ -74,6 +94,7 @@ class NvlinkCounters:
         self.tx_bytes = t1[0] - self.t0[0]
         self.rx_bytes = t1[1] - self.t0[1]
         self.links = t1[2]
+        self.field = t1[3]
 
 
 if __name__ == "__main__":

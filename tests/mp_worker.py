@@ -21,7 +21,7 @@ COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
 KIND_O = {th.RING: T.RING, th.DIRECT: T.DIRECT, th.SWITCH: T.SWITCH}
 
 
-def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None):
+def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None, lookahead=1):
     topo = th.Topology(sizes, bw, kinds)
     P = topo.P
     V = P // W
@@ -30,6 +30,7 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, ki
     comm = th.Comm(topo, N * esz, group=group)
     comm.set_engine(engine)
     comm.set_timeout(20.0)
+    comm.set_lookahead(lookahead)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy).bind(comm)
     xs = host_inputs(P, N, dtype, dist="wide")
     for v in range(V):
@@ -134,6 +135,9 @@ def nccl_and_stress_case(group, W, g, iters=60):
         if key not in plans:
             plans[key] = th.Plan(topo, th.ALLREDUCE, N * 4, C, pol, intra).bind(comm, ctas)
         comm.set_engine(eng)
+        # R28: ranks may run a dim's ops in different orders -- give every GPU
+        # its own intra-dim mode in the same collective (static / runtime L)
+        comm.set_lookahead([1, 4, 16, 32][(it + g) % 4])
         xs = [torch.randint(-(1 << 20), 1 << 20, (N,), dtype=torch.int32, device="cuda",
                             generator=torch.Generator(device="cuda").manual_seed(1000 * it + g * V + v))
               for v in range(V)]
@@ -324,7 +328,8 @@ def main():
         vec = 16 // ELEM_SIZE[dtype]
         cases.append((sizes, tuple(rng.choice([1, 2, 4]) for _ in range(D)), dtype, rng.choice([1, 4, 8]),
                       vec * rng.randint(1, 300), rng.choice([S.AR, S.AR, "RS", "AG"]),
-                      rng.choice([th.THEMIS, th.BASELINE]), "tma", kinds))
+                      rng.choice([th.THEMIS, th.BASELINE]), "tma", kinds,
+                      rng.choice([1, 4, 16])))
     fails = []
     for c in cases:
         if int(np.prod(c[0])) % W:

@@ -41,7 +41,8 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
-             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1, rotate=1):
+             intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1, rotate=1,
+             lookahead=1):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
@@ -51,6 +52,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_timeout(10.0)
     comm.set_min_cta_bytes(min_cta_bytes)
     comm.set_window_rotation(bool(rotate))
+    comm.set_lookahead(lookahead)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra, concurrency=concurrency).bind(comm, ctas)
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
@@ -513,6 +515,22 @@ def test_cuda_graph_capture_and_replay():
         comm.close()
 
 
+@pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), None), ((4, 2), None), ((2, 2, 2), (th.DIRECT, th.RING, th.DIRECT)),
+                                         ((3, 4), (th.RING, th.DIRECT))])
+@pytest.mark.parametrize("la", [2, 8, 32])
+def test_runtime_intra_dim_order(sizes, kinds, la):
+    """R28: producers pick the first ready op among the next L of the enforced
+    list (direct dims; ring dims keep the static order) — results stay
+    bit-exact against the oracle (every op's sum is order-independent), with
+    repeated calls, windows and mixed ring/direct dims; int32 and f32."""
+    P = int(np.prod(sizes))
+    kw = dict(kinds=kinds, lookahead=la, repeat=2)
+    check_ar(sizes, (1,) * len(sizes), "i32", 16, 4 * 300, **kw)
+    check_ar(sizes, (4,) + (1,) * (len(sizes) - 1), "f32", 16, 4 * 301, dist="wide", **kw)
+    check_ar(sizes, (1,) * len(sizes), "i32", 8, 4 * 64, min_cta_bytes=4096, ctas=[6] * len(sizes), **kw)
+    assert P >= 8
+
+
 def test_max_ranks_and_many_chunks():
     """Edge sizes on the executor: 64 logical ranks (2^6, the per-comm
     maximum) in one GPU, and 1024 chunks (THEMIS_MAX_CHUNKS) on 2x2x2 —
@@ -583,13 +601,15 @@ def test_random_executor_configs():
         vec = 16 // ELEM_SIZE[dtype]
         slice_elems = vec * rng.randint(1, 700)
         ctas = [rng.randint(max(2, conc), 24) for _ in range(D)]
+        la = rng.choice([1, 1, 4, 16])
         kw = dict(kinds=kinds, ctas=ctas, intra=intra, concurrency=conc, min_cta_bytes=0 if conc > 1 else mcb,
-                  dist="wide" if dtype != "i32" else "recipe")
+                  dist="wide" if dtype != "i32" else "recipe", lookahead=la)
         try:
             check_ar(tuple(sizes), bw, dtype, C_, slice_elems, policy, **kw)
         except AssertionError as e:
             raise AssertionError(f"case {i}: sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy} "
-                                 f"intra {intra} conc {conc} mcb {mcb} slice {slice_elems} ctas {ctas}: {e}")
+                                 f"intra {intra} conc {conc} mcb {mcb} slice {slice_elems} ctas {ctas} "
+                                 f"lookahead {la}: {e}")
 
 
 def test_random_rs_ag_configs():
