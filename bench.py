@@ -133,10 +133,34 @@ def hbm_bytes_per_rank(plan, S):
     return tot
 
 
-def nvlink_bytes_per_rank(plan, cross):
-    """Bytes a rank pulls from other GPUs: N_K over the cross-GPU dims."""
-    vol = plan.info["dim_volume"]
-    return sum(vol[k] for k in cross) / plan.info["byte_scale"]
+def remote_fraction(sizes, n_gpus, k, q, ring=False):
+    """Share of logical rank q's dim-k pulls that cross to another GPU: the
+    direct algorithm pulls equally from its P_k - 1 dim peers, the ring only
+    from its left neighbour (rank r lives on GPU r // V)."""
+    P = 1
+    for s_ in sizes:
+        P *= s_
+    V = P // n_gpus
+    stride = 1
+    for s_ in sizes[:k]:
+        stride *= s_
+    pk = sizes[k]
+    c = (q // stride) % pk
+    peer = lambda j: q + (j - c) * stride
+    if ring:
+        return float(peer((c - 1) % pk) // V != q // V)
+    return sum(peer(j) // V != q // V for j in range(pk) if j != c) / (pk - 1)
+
+
+def nvlink_bytes_per_gpu(plan, sizes, n_gpus, ring_dims=()):
+    """Bytes one GPU pulls over NVLink per collective (max over GPUs): its V
+    ranks' N_K, each weighted by the share of dim-K peers on other GPUs."""
+    vol = [v / plan.info["byte_scale"] for v in plan.info["dim_volume"]]
+    P = plan.info["n_ranks"]
+    V = P // n_gpus
+    return max(sum(vol[k] * remote_fraction(sizes, n_gpus, k, q, k in ring_dims)
+                   for q in range(g * V, (g + 1) * V) for k in range(len(sizes)))
+               for g in range(n_gpus))
 
 
 def run_themis(a):
@@ -180,7 +204,7 @@ def run_themis(a):
         stages, stage_kb = a.stages or 3, a.stage_kb or 64
     else:
         stages, stage_kb = a.stages or 4, a.stage_kb or 48
-    kinds = (th.SWITCH,) * len(SIZES) if a.nvls else None   # NVSwitch dims: in-switch reduction where eligible (R27)
+    kinds = (th.NVLS,) * len(SIZES) if a.nvls else None   # NVSwitch dims with in-switch reduction where eligible (R27, R29)
     topo = th.Topology(SIZES, ratio, kinds)
     comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
     comm.set_timeout(30.0)
@@ -427,7 +451,7 @@ def run_themis(a):
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_bytes = V * hbm_bytes_per_rank(main, S)
-    nvl_bytes = V * nvlink_bytes_per_rank(main, lay["cross_gpu_dims"])
+    nvl_bytes = nvlink_bytes_per_gpu(main, SIZES, world)
     hbm_ach = hbm_bytes / t_main / 1e9
     nvl_ach = nvl_bytes / t_main / 1e9
     if world == 1 or hbm_ach / hbm_peak >= nvl_ach / NVLINK_PEAK:

@@ -63,15 +63,24 @@ typedef enum { THEMIS_POLICY_BASELINE = 0, THEMIS_POLICY_THEMIS = 1 } themis_pol
 /* Intra-dimension order: SCF keyed on the op's transfer volume
  * (R9), FIFO (R10), or SCF keyed on bytes-before (SPEC.md:330 literal). */
 typedef enum { THEMIS_INTRA_SCF = 0, THEMIS_INTRA_FIFO = 1, THEMIS_INTRA_SCF_LITERAL = 2 } themis_intra_t;
-/* Table 1: per-dimension topology -> basic algorithm. */
-typedef enum { THEMIS_DIM_RING = 0, THEMIS_DIM_DIRECT = 1, THEMIS_DIM_SWITCH = 2 } themis_dim_kind_t;
+/* Table 1: per-dimension topology -> basic algorithm.
+ * THEMIS_DIM_NVLS (extension, PAPER.md:493-494 in-network offload; DESIGN R29):
+ * a Switch dim whose switch reduces.  The latency model runs an All-Reduce
+ * chunk's last RS stage + first AG stage on it (the same dim, Algorithm 1 line
+ * 8) as ONE op of n = (1 + 1/P_k) x bytes-held (each member's copy into the
+ * switch + the multicast of the reduced piece) and 2 steps of latency; the AG
+ * half becomes a zero-volume op.  Bound to a comm with a multicast heap whose
+ * dim group is one rank per GPU (P_k == W, stride_k == V), the executor runs
+ * the pair in the switch (multimem.ld_reduce + multimem.st); otherwise as
+ * direct RS + AG (same result, themis_plan_bound_nvls reports 0). */
+typedef enum { THEMIS_DIM_RING = 0, THEMIS_DIM_DIRECT = 1, THEMIS_DIM_SWITCH = 2, THEMIS_DIM_NVLS = 3 } themis_dim_kind_t;
 
 /* Logical topology P_1 x ... x P_D.  Rank r has coordinates
  * c_k = floor(r / prod_{i<k} P_i) mod P_k (dim1 fastest, R15).
  * bw[k]: aggregate uni-directional per-NPU bandwidth of dim k in MB/s
  * (PAPER.md:505, :136); with zero latencies only the ratios matter.
  * Validation: 1 <= ndims <= 8, size >= 2, bw > 0,
- * SWITCH => size is a power of two. */
+ * SWITCH / NVLS => size is a power of two. */
 typedef struct {
   int32_t ndims;
   int32_t size[THEMIS_MAX_DIMS];
@@ -305,6 +314,10 @@ themis_status_t themis_plan_bind(themis_plan_t* plan, themis_comm_t* comm, const
  * Errors: PLAN_MISMATCH if the plan is not bound. */
 themis_status_t themis_plan_launch_hash(const themis_plan_t* plan, uint64_t count, int32_t dtype,
                                         uint64_t* hash /*[host,out]*/);
+/* Number of a bound plan's chunk RS+AG pairs that run as in-switch
+ * All-Reduces (NVLS dims on a multicast-capable comm, R29); 0 otherwise.
+ * Errors: PLAN_MISMATCH if the plan is not bound. */
+themis_status_t themis_plan_bound_nvls(const themis_plan_t* plan, int32_t* n_pairs /*[host,out]*/);
 /* CTAs per dimension group a bound plan launches with ([host, out] D entries).
  * Errors: PLAN_MISMATCH if the plan is not bound. */
 themis_status_t themis_plan_bound_ctas(const themis_plan_t* plan, int32_t* ctas_per_dim /*[host,out]*/);

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 from fractions import Fraction
 
-from .topology import DIRECT, RING, SWITCH, Dim
+from .topology import DIRECT, NVLS, RING, SWITCH, Dim
 
 RS, AG = "RS", "AG"
 
@@ -29,7 +29,7 @@ def num_steps(phase: str, kind: str, p: int) -> int:
         return p - 1
     if kind == DIRECT:
         return 1
-    if kind == SWITCH:
+    if kind in (SWITCH, NVLS):
         if p & (p - 1):
             raise ValueError("halving-doubling needs a power of two")
         return p.bit_length() - 1
@@ -59,3 +59,32 @@ def fixed_delay(dim: Dim, phase: str) -> Fraction:
 def chunk_load(dim: Dim, phase: str, bytes_before) -> Fraction:
     """Latency-model increment n_K^i x B_K with B_K = 1/BW_K."""
     return bytes_sent(phase, dim.size, bytes_before) / dim.bw
+
+
+# ---- in-network offload (PAPER.md:493-494: "Switch collective offload reduces
+# the collective's network traffic (n_K^i) and fixed delay (A_K)"; the
+# hierarchical structure and Themis's balancing stay).  Reading R29: on an NVLS
+# dim an All-Reduce chunk's last RS stage and its first AG stage (the same dim,
+# Algorithm 1 line 8) run as ONE in-switch All-Reduce of the stage's data.  Per
+# NPU, holding b bytes before the pair, each member sends its copy of every
+# member's piece into the switch (b) and the reduced piece back for the
+# multicast (b/p): n = (1 + 1/p) * b, in 2 switch traversals (reduce, then
+# multicast store).  The AG half is then a zero-volume op that only orders the
+# chunk's pipeline.
+
+FUSED_STEPS = 2
+
+
+def fused_bytes_sent(p: int, bytes_before) -> Fraction:
+    """n_K^i of the fused in-switch RS+AG pair on a dim of size p."""
+    b = Fraction(bytes_before)
+    return b + b / p
+
+
+def fused_delay(dim: Dim) -> Fraction:
+    return FUSED_STEPS * dim.step_latency
+
+
+def is_fused(topo, coll: str, rs, ag) -> bool:
+    """AR chunk whose last RS dim is its first AG dim and an NVLS dim (R29)."""
+    return coll == "AR" and bool(rs) and bool(ag) and rs[-1] == ag[0] and topo.dims[rs[-1]].kind == NVLS

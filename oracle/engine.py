@@ -30,7 +30,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from fractions import Fraction
 
-from .collectives import AG, RS, bytes_sent, fixed_delay, size_after
+from .collectives import AG, RS, bytes_sent, fixed_delay, fused_bytes_sent, fused_delay, is_fused, size_after
 from .scheduler import AR, Schedule
 
 FIFO, SCF, SCF_LITERAL = "fifo", "scf", "scf_literal"
@@ -68,11 +68,18 @@ def chunk_ops(sched: Schedule, charge_latency: bool = False, servers: int = 1) -
     out = []
     for cs in sched.chunks:
         b = sched.chunk_bytes if cs.rs else sched.chunk_bytes / topo.P
+        fused = is_fused(topo, sched.coll, cs.rs, cs.ag)
         ops = []
         for s, (d, ph) in enumerate(cs.stages()):
             dim = topo.dims[d]
-            v = bytes_sent(ph, dim.size, b)
-            dur = v / dim.bw * servers + (fixed_delay(dim, ph) if charge_latency else 0)
+            if fused and s == len(cs.rs) - 1:       # in-switch RS+AG pair (R29)
+                v = fused_bytes_sent(dim.size, b)
+                dur = v / dim.bw * servers + (fused_delay(dim) if charge_latency else 0)
+            elif fused and s == len(cs.rs):         # its AG half: dependency only
+                v, dur = Fraction(0), Fraction(0)
+            else:
+                v = bytes_sent(ph, dim.size, b)
+                dur = v / dim.bw * servers + (fixed_delay(dim, ph) if charge_latency else 0)
             ops.append(Op(cs.chunk, s, d, ph, b, v, dur))
             b = size_after(ph, dim.size, b)
         out.append(ops)
@@ -180,7 +187,9 @@ def simulate(sched: Schedule, policy: str = SCF, charge_latency: bool = False,
 
 
 def ideal_time(sched: Schedule) -> Fraction:
-    """Volume-based Ideal (reading R13): algorithmic bytes per NPU / sum BW."""
+    """Volume-based Ideal (reading R13): algorithmic bytes per NPU / sum BW
+    of the host-driven algorithms (a lower bound only without NVLS dims,
+    whose in-switch pairs send less, R29)."""
     topo = sched.topo
     f = Fraction(topo.P - 1, topo.P) * sched.total_bytes
     if sched.coll == AR:

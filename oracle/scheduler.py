@@ -39,8 +39,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from fractions import Fraction
 
-from .collectives import AG, RS, chunk_load, fixed_delay, size_after
-from .topology import Topology
+from .collectives import AG, RS, chunk_load, fixed_delay, fused_bytes_sent, fused_delay, is_fused, size_after
+from .topology import NVLS, Topology
 
 AR = "AR"
 BASELINE, THEMIS = "baseline", "themis"
@@ -76,7 +76,8 @@ def tracker_reset(topo: Topology, coll: str) -> list:
     """DimLoadTracker.reset(CT): each load starts at A_K of the phases the
     collective will run (reading R7)."""
     phases = {AR: (RS, AG), RS: (RS,), AG: (AG,)}[coll]
-    return [sum((fixed_delay(d, ph) for ph in phases), Fraction(0)) for d in topo.dims]
+    return [fused_delay(d) if coll == AR and d.kind == NVLS else
+            sum((fixed_delay(d, ph) for ph in phases), Fraction(0)) for d in topo.dims]    # R29
 
 
 def baseline_order(topo: Topology, ct: str) -> tuple:
@@ -96,6 +97,21 @@ def walk_loads(topo: Topology, ct: str, order, bytes_before) -> tuple:
         inc[d] += chunk_load(dim, ct, b)
         b = size_after(ct, dim.size, b)
     return inc, b
+
+
+def ar_walk(topo: Topology, rs, ag, chunk) -> list:
+    """An All-Reduce chunk's tracker increments: the RS walk then the AG walk
+    (R1); on an NVLS dim the last RS + first AG stage is one in-switch
+    All-Reduce of n = (1 + 1/p) b bytes (R29)."""
+    if is_fused(topo, AR, rs, ag):
+        inc_rs, b = walk_loads(topo, RS, rs[:-1], chunk)
+        k = rs[-1]
+        inc_rs[k] += fused_bytes_sent(topo.dims[k].size, b) / topo.dims[k].bw
+        inc_ag, _ = walk_loads(topo, AG, ag[1:], b)
+    else:
+        inc_rs, b = walk_loads(topo, RS, rs, chunk)
+        inc_ag, _ = walk_loads(topo, AG, ag, b)
+    return [x + y for x, y in zip(inc_rs, inc_ag)]
 
 
 def threshold(topo: Topology, loads, chunk_bytes, threshold_div) -> Fraction:
@@ -136,9 +152,7 @@ def schedule_collective(topo: Topology, coll: str, total_bytes, n_chunks: int,
             else:
                 rs, greedy = baseline_order(topo, RS), False
             ag = tuple(reversed(rs))                        # line 8
-            inc_rs, b = walk_loads(topo, RS, rs, chunk)
-            inc_ag, _ = walk_loads(topo, AG, ag, b)
-            inc = [x + y for x, y in zip(inc_rs, inc_ag)]   # reading R1
+            inc = ar_walk(topo, rs, ag, chunk)              # reading R1 (+ R29)
             cs = ChunkSchedule(i, rs, ag)
         else:
             if policy == THEMIS:
@@ -161,9 +175,15 @@ def dim_volumes(sched: Schedule) -> list:
     chunk = sched.chunk_bytes
     for cs in sched.chunks:
         b = chunk if cs.rs else chunk / topo.P
-        for d, ph in cs.stages():
+        fused = is_fused(topo, sched.coll, cs.rs, cs.ag)
+        for i, (d, ph) in enumerate(cs.stages()):
             p = topo.dims[d].size
-            N[d] += Fraction(p - 1, p) * b if ph == RS else (p - 1) * b
+            if fused and i == len(cs.rs) - 1:            # the in-switch pair (R29)
+                N[d] += fused_bytes_sent(p, b)
+            elif fused and i == len(cs.rs):
+                pass
+            else:
+                N[d] += Fraction(p - 1, p) * b if ph == RS else (p - 1) * b
             b = size_after(ph, p, b)
     return N
 

@@ -22,7 +22,10 @@ from fractions import Fraction
 from typing import Sequence
 
 RING, DIRECT, SWITCH = "ring", "direct", "switch"   # Table 1
-KINDS = (RING, DIRECT, SWITCH)
+# A Switch dimension whose switch can reduce (in-network collective offload,
+# PAPER.md:493-494; on B200: NVSwitch NVLS multimem).  DESIGN.md reading R29.
+NVLS = "nvls"
+KINDS = (RING, DIRECT, SWITCH, NVLS)
 
 
 def gbps(x) -> Fraction:
@@ -85,7 +88,7 @@ class Topology:
                 raise ValueError(f"dim{i+1}: negative latency")
             if d.kind not in KINDS:
                 raise ValueError(f"dim{i+1}: unknown kind {d.kind!r}")
-            if d.kind == SWITCH and (d.size & (d.size - 1)):
+            if d.kind in (SWITCH, NVLS) and (d.size & (d.size - 1)):
                 raise ValueError(f"dim{i+1}: switch size {d.size} not a power of two")
 
     # --- rank coordinates (dim1 fastest) ---------------------------------

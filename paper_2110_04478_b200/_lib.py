@@ -86,6 +86,7 @@ SIGNATURES = {
     "themis_default_ctas": (_ST, [C.POINTER(Topology_t), C.c_int32, _P]),
     "themis_plan_bind": (_ST, [_P, _P, _P]),
     "themis_plan_bound_ctas": (_ST, [_P, _P]),
+    "themis_plan_bound_nvls": (_ST, [_P, C.POINTER(C.c_int32)]),
     "themis_plan_launch_hash": (_ST, [_P, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]),
     "themis_allreduce": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),
     "themis_reduce_scatter": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),

@@ -87,6 +87,7 @@ struct themis_comm {
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
   int lookahead = 1;           // runtime intra-dim order window (themis_comm_set_lookahead); 1 = static
+  uint32_t exp = 0;            // experiment bits (env THEMIS_EXP)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -109,6 +110,7 @@ struct BindState {
   int32_t total_ctas = 0;
   bool nvls = false;  // some op runs through the switch (TMA engine only)
   uint32_t dyn_mask = 0;  // dims whose ops may take the runtime order (direct algorithm, no NVLS op)
+  int32_t nvls_pairs = 0;  // RS+AG pairs running in the switch
   uint64_t desc_hash = 0;  // of the uploaded op windows / algorithms (mixed into the launch's plan hash)
 };
 }  // namespace themis
@@ -217,6 +219,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     c->stages = std::max(1, std::min(std::min(kStages, kStages * kStageBytes / c->stage_bytes), atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   if (const char* env = getenv("THEMIS_WINDOW_ROTATE")) c->window_rotate = atoi(env) != 0;
+  if (const char* env = getenv("THEMIS_EXP")) c->exp = (uint32_t)strtoul(env, nullptr, 0);
   if (const char* env = getenv("THEMIS_LOOKAHEAD")) c->lookahead = std::max(1, std::min(kMaxLookahead, atoi(env)));
   c->max_blocks = nb * c->num_sms;
   *out = c;
@@ -383,17 +386,19 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     d.ring = pl->topo.kind[o.dim] == THEMIS_DIM_RING && pl->topo.size[o.dim] >= 3;
     ops[i] = d;
   }
-  // NVLS (R27): on a switch dim whose group is one rank per GPU at the same
-  // local index (P_k == W, stride_k == V) and a comm with a multicast mapping,
-  // an RS op immediately followed by the chunk's AG op on the same dim runs as
-  // one in-switch All-Reduce of the own piece (multimem.ld_reduce + multimem.st);
-  // the AG op then only carries the dependency.
+  // NVLS (R27, R29): on an NVLS dim whose group is one rank per GPU at the
+  // same local index (P_k == W, stride_k == V) and a comm with a multicast
+  // mapping, an RS op immediately followed by the chunk's AG op on the same dim
+  // (the pair the planner modelled as one in-switch All-Reduce) runs as one
+  // in-switch All-Reduce of the own piece (multimem.ld_reduce + multimem.st);
+  // the AG op then only carries the dependency.  Ineligible: direct RS + AG.
   bool any_nvls = false;
+  int n_fused = 0;
   if (c->mc_heap) {
     int64_t stride = 1;
     bool elig[THEMIS_MAX_DIMS] = {};
     for (int k = 0; k < D; ++k) {
-      elig[k] = pl->topo.kind[k] == THEMIS_DIM_SWITCH && pl->topo.size[k] == c->W && stride == c->V && c->W > 1;
+      elig[k] = pl->topo.kind[k] == THEMIS_DIM_NVLS && pl->topo.size[k] == c->W && stride == c->V && c->W > 1;
       stride *= pl->topo.size[k];
     }
     for (int ch = 0; ch < pl->C; ++ch)
@@ -405,6 +410,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
           ops[i].nvls = 1;
           ops[i + 1].nvls = 2;
           any_nvls = true;
+          ++n_fused;
         }
       }
   }
@@ -491,11 +497,18 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   }
   b->total_ctas = tot;
   b->nvls = any_nvls;
+  b->nvls_pairs = n_fused;
   b->dyn_mask = (1u << D) - 1;
   for (const OpDesc& d : ops)
     if (d.ring || d.nvls) b->dyn_mask &= ~(1u << d.dim);
   pl->bind = b;
   c->bound.push_back(pl);
+  return THEMIS_OK;
+}
+
+extern "C" themis_status_t themis_plan_bound_nvls(const themis_plan_t* pl, int32_t* n_pairs) {
+  if (!pl || !pl->bind || !n_pairs) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan not bound");
+  *n_pairs = pl->bind->nvls_pairs;
   return THEMIS_OK;
 }
 
@@ -594,6 +607,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   kp.plan_hash = launch_hash(pl, count, dtype);
   kp.lookahead = c->lookahead;
+  kp.exp = c->exp;
   kp.dyn_mask = pl->bind->dyn_mask;
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;

@@ -66,6 +66,7 @@ struct KParams {
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
   uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
+  uint32_t exp;             // experiment bits (env THEMIS_EXP; 0 = the documented protocol)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
@@ -428,6 +429,17 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
   return ok;
 }
 
+// Hand a ring slot back to the producer after this warp's reads of it.
+// Default: a release arrive (the reads happen-before the producer's acquire and
+// its next TMA write into the slot).  Experiment bit 0 (THEMIS_EXP=1): relaxed
+// arrive (the reads' values were already consumed by the stores before it).
+__device__ __forceinline__ void slot_release(const KParams& p, uint64_t* bar) {
+  if (p.exp & 1u)
+    dev::mbar_arrive_relaxed(bar);
+  else
+    dev::mbar_arrive(bar);
+}
+
 // Consumers: returns false if the kernel is aborting (watchdog).
 template <class Tag>
 __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
@@ -460,7 +472,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         for (; w < w1; w += kCons) dev::mc_st(mc + 16 * w, dev::mc_ld_reduce<Tag>(mc + 16 * w));
       });
     __syncwarp();
-    if (lane == 0) dev::mbar_arrive(&empty[s]);
+    if (lane == 0) slot_release(p, &empty[s]);
     ++ctr;
     return true;
   }
@@ -484,7 +496,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
           uint4* dj = reinterpret_cast<uint4*>(base + pos + (uint64_t)peer_member(j, ck) * ps);
           for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dj + w, sm[w]);
           __syncwarp();
-          if (lane == 0) dev::mbar_arrive(&empty[s]);  // release: the slot's reads happen-before the producer's next TMA write
+          if (lane == 0) slot_release(p, &empty[s]);
         }
       }
       return;
@@ -516,7 +528,7 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         for (uint32_t w = ct; w < n16; w += kCons) dev::st_v4(dst + w, sm[w]);
       }
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);  // release: the slot's reads happen-before the producer's next TMA write
+      if (lane == 0) slot_release(p, &empty[s]);
     }
   });
   return ok;

@@ -63,8 +63,8 @@ themis_status_t validate(const themis_topology_t* t, const themis_plan_req_t* r)
   for (int k = 0; k < t->ndims; ++k) {
     if (t->size[k] < 2) return fail(THEMIS_ERR_INVALID_ARG, "dim" + std::to_string(k + 1) + ": size < 2");
     if (t->bw_mbps[k] == 0) return fail(THEMIS_ERR_INVALID_ARG, "dim" + std::to_string(k + 1) + ": bw == 0");
-    if (t->kind[k] < 0 || t->kind[k] > 2) return fail(THEMIS_ERR_INVALID_ARG, "bad dim kind");
-    if (t->kind[k] == THEMIS_DIM_SWITCH && (t->size[k] & (t->size[k] - 1)))
+    if (t->kind[k] < 0 || t->kind[k] > 3) return fail(THEMIS_ERR_INVALID_ARG, "bad dim kind");
+    if ((t->kind[k] == THEMIS_DIM_SWITCH || t->kind[k] == THEMIS_DIM_NVLS) && (t->size[k] & (t->size[k] - 1)))
       return fail(THEMIS_ERR_INVALID_ARG, "dim" + std::to_string(k + 1) + ": switch size not a power of two");
     P *= (uint64_t)t->size[k];
     if (P > (1u << 20)) return fail(THEMIS_ERR_INVALID_ARG, "more than 2^20 ranks");
@@ -93,7 +93,15 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
 struct Planner {
   themis_plan_t& pl;
   int D, C, P;
-  u128 lambda, g_bytes = 1, W[THEMIS_MAX_DIMS], A_rs[THEMIS_MAX_DIMS], A_ag[THEMIS_MAX_DIMS];
+  u128 lambda, g_bytes = 1, W[THEMIS_MAX_DIMS], A_rs[THEMIS_MAX_DIMS], A_ag[THEMIS_MAX_DIMS],
+      A_fused[THEMIS_MAX_DIMS];
+  // DimLoadTracker.reset(CT): A_K of the collective on dim k
+  u128 seed(int k) const {
+    const int coll = pl.req.coll;
+    if (coll == THEMIS_ALLREDUCE)
+      return pl.topo.kind[k] == THEMIS_DIM_NVLS ? A_fused[k] : A_rs[k] + A_ag[k];  // R29
+    return coll == THEMIS_REDUCE_SCATTER ? A_rs[k] : A_ag[k];
+  }
   u128 chunk_scaled() const { return (u128)pl.req.bytes / g_bytes * P; }  // (S/C) * P*C/g
 
   explicit Planner(themis_plan_t& p) : pl(p), D(p.D), C(p.C), P(p.P) {}
@@ -115,6 +123,7 @@ struct Planner {
       u128 lat = (u128)pl.topo.step_latency_ns[k] * pl.time_scale;
       A_rs[k] = (u128)num_steps(pl.topo.kind[k], pl.topo.size[k]) * lat;
       A_ag[k] = A_rs[k];  // same step count per phase (R7)
+      A_fused[k] = (u128)2 * lat;  // in-switch RS+AG pair: reduce + multicast traversals (R29)
     }
     u128 top = (u128)pl.req.bytes * P * 1000 * 16 * 1024;
     for (int k = 0; k < D; ++k)
@@ -127,8 +136,8 @@ struct Planner {
   static u128 ag_vol(u128 b, int p) { return b * (p - 1); }
 
   // Walk a chunk through `order` (phase ph), adding n_K^i * W_K to inc.
-  void walk(int ph, const uint8_t* order, u128 b, u128* inc, u128* b_out) const {
-    for (int i = 0; i < D; ++i) {
+  void walk(int ph, const uint8_t* order, u128 b, u128* inc, u128* b_out, int n = -1) const {
+    for (int i = 0; i < (n < 0 ? D : n); ++i) {
       int d = order[i];
       int p = pl.topo.size[d];
       if (ph == 0) {
@@ -140,6 +149,27 @@ struct Planner {
       }
     }
     if (b_out) *b_out = b;
+  }
+
+  // R29: an All-Reduce chunk whose last RS dim is its first AG dim and an
+  // NVLS dim runs that pair as one in-switch All-Reduce.
+  bool fused(const uint8_t* rs, const uint8_t* ag) const {
+    return pl.req.coll == THEMIS_ALLREDUCE && rs[D - 1] == ag[0] && pl.topo.kind[rs[D - 1]] == THEMIS_DIM_NVLS;
+  }
+  // n = (1 + 1/p) b of the fused pair (b = bytes held before it)
+  static u128 fused_vol(u128 b, int p) { return b + b / p; }
+  // AR tracker increments: RS walk + AG walk (R1), the fused pair as one op (R29)
+  void ar_walk(const uint8_t* rs, const uint8_t* ag, u128 chunk, u128* inc) const {
+    u128 b;
+    if (fused(rs, ag)) {
+      walk(0, rs, chunk, inc, &b, D - 1);
+      const int k = rs[D - 1];
+      inc[k] += fused_vol(b, pl.topo.size[k]) * W[k];
+      walk(1, ag + 1, b, inc, nullptr, D - 1);
+    } else {
+      walk(0, rs, chunk, inc, &b);
+      walk(1, ag, b, inc, nullptr);
+    }
   }
 
   // SCHEDULER.SCHEDULE lines 18-27 (ct: 0 RS, 1 AG); returns true if greedy.
@@ -170,8 +200,7 @@ struct Planner {
   void algorithm1() {
     const int coll = pl.req.coll;
     u128 L[THEMIS_MAX_DIMS];
-    for (int k = 0; k < D; ++k)  // DimLoadTracker.reset(CT)
-      L[k] = coll == THEMIS_ALLREDUCE ? A_rs[k] + A_ag[k] : coll == THEMIS_REDUCE_SCATTER ? A_rs[k] : A_ag[k];
+    for (int k = 0; k < D; ++k) L[k] = seed(k);  // DimLoadTracker.reset(CT)
     const u128 chunk = chunk_scaled();  // CS/CPC x byte_scale
     pl.rs.assign((size_t)C * D, 0xFF);
     pl.ag.assign((size_t)C * D, 0xFF);
@@ -183,9 +212,7 @@ struct Planner {
       if (coll == THEMIS_ALLREDUCE) {
         pl.n_greedy += schedule_one(0, L, chunk, rs);
         for (int k = 0; k < D; ++k) ag[k] = rs[D - 1 - k];  // line 8
-        u128 b;
-        walk(0, rs, chunk, inc, &b);
-        walk(1, ag, b, inc, nullptr);  // RS + AG charged (R1)
+        ar_walk(rs, ag, chunk, inc);  // RS + AG charged (R1), NVLS pair fused (R29)
       } else if (coll == THEMIS_REDUCE_SCATTER) {
         pl.n_greedy += schedule_one(0, L, chunk, rs);
         walk(0, rs, chunk, inc, nullptr);
@@ -204,8 +231,7 @@ struct Planner {
   void custom_orders(const uint8_t* rs_in, const uint8_t* ag_in) {
     const int coll = pl.req.coll;
     u128 L[THEMIS_MAX_DIMS];
-    for (int k = 0; k < D; ++k)
-      L[k] = coll == THEMIS_ALLREDUCE ? A_rs[k] + A_ag[k] : coll == THEMIS_REDUCE_SCATTER ? A_rs[k] : A_ag[k];
+    for (int k = 0; k < D; ++k) L[k] = seed(k);
     const u128 chunk = chunk_scaled();
     pl.rs.assign((size_t)C * D, 0xFF);
     pl.ag.assign((size_t)C * D, 0xFF);
@@ -216,20 +242,22 @@ struct Planner {
       uint8_t* ag = &pl.ag[(size_t)c * D];
       bool differs = false;
       u128 b = coll == THEMIS_ALL_GATHER ? chunk / P : chunk;
-      if (coll != THEMIS_ALL_GATHER) {
+      if (coll != THEMIS_ALL_GATHER)
         for (int k = 0; k < D; ++k) {
           rs[k] = rs_in[(size_t)c * D + k];
           differs |= rs[k] != k;
         }
-        walk(0, rs, b, inc, &b);
-      }
-      if (coll != THEMIS_REDUCE_SCATTER) {
+      if (coll != THEMIS_REDUCE_SCATTER)
         for (int k = 0; k < D; ++k) {
           ag[k] = ag_in[(size_t)c * D + k];
           differs |= ag[k] != D - 1 - k;
         }
+      if (coll == THEMIS_ALLREDUCE)
+        ar_walk(rs, ag, b, inc);
+      else if (coll == THEMIS_REDUCE_SCATTER)
+        walk(0, rs, b, inc, nullptr);
+      else
         walk(1, ag, b, inc, nullptr);
-      }
       pl.n_greedy += differs;
       for (int k = 0; k < D; ++k) L[k] += inc[k];
     }
@@ -247,6 +275,7 @@ struct Planner {
         b /= P;
         red = (1u << D) - 1;
       }
+      const bool fz = coll == THEMIS_ALLREDUCE && fused(&pl.rs[(size_t)c * D], &pl.ag[(size_t)c * D]);
       for (int s = 0; s < pl.NS; ++s) {
         Op op{};
         op.chunk = c;
@@ -258,8 +287,11 @@ struct Planner {
         op.reduced_before = red;
         op.bytes_before = b;
         op.volume = is_rs ? rs_vol(b, p) : ag_vol(b, p);
+        if (fz && s == D - 1) op.volume = fused_vol(b, p);  // the in-switch pair (R29)
+        if (fz && s == D) op.volume = 0;                    // its AG half: dependency only
         op.duration = op.volume * W[op.dim] * (u128)std::max(1, pl.req.concurrency);  // BW_K / servers
-        if (pl.req.charge_latency) op.duration += is_rs ? A_rs[op.dim] : A_ag[op.dim];
+        if (pl.req.charge_latency && !(fz && s == D))
+          op.duration += fz && s == D - 1 ? A_fused[op.dim] : is_rs ? A_rs[op.dim] : A_ag[op.dim];
         if (is_rs) {
           b /= p;
           red |= 1u << op.dim;

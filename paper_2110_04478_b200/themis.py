@@ -20,6 +20,7 @@ from ._lib import (IPC_HANDLE_BYTES, MAX_DIMS, MAX_GPUS, PlanInfo_t, PlanReq_t, 
                    lib)
 
 RING, DIRECT, SWITCH = 0, 1, 2                 # Table 1
+NVLS = 3                                       # switch with in-switch reduction (R29)
 ALLREDUCE, REDUCE_SCATTER, ALL_GATHER = 0, 1, 2
 BASELINE, THEMIS = 0, 1                        # Table 3
 SCF, FIFO, SCF_LITERAL = 0, 1, 2               # §4.3
@@ -199,6 +200,12 @@ class Plan:
         check(lib().themis_plan_bind(self.h, comm.h, arr))
         self.comm = comm
         return self
+
+    def bound_nvls(self) -> int:
+        """RS+AG pairs of this bound plan that run in the switch (R29)."""
+        n = C.c_int32()
+        check(lib().themis_plan_bound_nvls(self.h, C.byref(n)))
+        return n.value
 
     def bound_ctas(self) -> list:
         arr = (C.c_int32 * MAX_DIMS)()
@@ -529,5 +536,5 @@ def version() -> str:
 
 __all__ = ["Topology", "Plan", "Comm", "themis_plan", "themis_allreduce", "themis_reduce_scatter",
            "themis_all_gather", "themis_allreduce_host", "run", "heap_layout", "default_ctas", "ThemisError",
-           "RING", "DIRECT", "SWITCH", "ALLREDUCE", "REDUCE_SCATTER", "ALL_GATHER", "BASELINE", "THEMIS", "SCF",
+           "RING", "DIRECT", "SWITCH", "NVLS", "ALLREDUCE", "REDUCE_SCATTER", "ALL_GATHER", "BASELINE", "THEMIS", "SCF",
            "FIFO", "SCF_LITERAL", "DTYPES", "ELEM_SIZE"]

@@ -222,11 +222,11 @@ def api_case(group, W, g):
 
 
 def nvls_case(group, W, g):
-    """NVLS switch dims (R27) on a multicast heap: int32 exact vs the plain
+    """NVLS dims (R27, R29) on a multicast heap: int32 exact vs the plain
     definition; floats within the north_star tolerance of the fp64 sum (the
     switch sums in its own order) and identical on every rank.  Returns the
     number of mismatches (-1 if this box has no multicast)."""
-    SW, DI = th.SWITCH, th.DIRECT
+    SW, DI = th.NVLS, th.DIRECT
     cfgs = [((W,), (SW,), "i32", 8), ((W,), (SW,), "f32", 8), ((2, W), (DI, SW), "f32", 4),
             ((2, W), (DI, SW), "bf16", 4)]
     if W == 2:
@@ -243,6 +243,7 @@ def nvls_case(group, W, g):
             return -1
         comm.set_timeout(20.0)
         plan = th.Plan(topo, th.ALLREDUCE, N * ELEM_SIZE[dtype], C).bind(comm)
+        bad += int(plan.bound_nvls() == 0)       # the modelled in-switch pairs really run in the switch
         xs = host_inputs(P, N, dtype)
         for v in range(V):
             src = torch.from_numpy(xs[g * V + v].view(np.int16) if dtype == "bf16" else xs[g * V + v])

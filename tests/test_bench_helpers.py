@@ -22,7 +22,20 @@ def test_nvlink_bytes_equal_bus_bytes_at_one_rank_per_gpu():
     p = th.Plan(th.Topology((2, 2, 2), (4, 2, 1)), th.ALLREDUCE, S, 64)
     lay = bench.logical_layout((2, 2, 2), 8)
     assert lay["V"] == 1 and lay["cross_gpu_dims"] == [0, 1, 2]
-    assert bench.nvlink_bytes_per_rank(p, lay["cross_gpu_dims"]) == 2 * S * 7 / 8
+    assert bench.nvlink_bytes_per_gpu(p, (2, 2, 2), 8) == 2 * S * 7 / 8
+    assert bench.nvlink_bytes_per_gpu(p, (2, 2, 2), 1) == 0
+    p.close()
+
+
+def test_nvlink_bytes_straddling_dim():
+    """4x2 on 4 GPUs (V = 2): dim1's group {0,1,2,3} spans GPUs {0,0,1,1}, so
+    2 of each rank's 3 dim1 peers are remote; dim2's peer is always remote."""
+    S = 1 << 30
+    p = th.Plan(th.Topology((4, 2), (1, 1)), th.ALLREDUCE, S, 64)
+    n1, n2 = [v / p.info["byte_scale"] for v in p.info["dim_volume"]]
+    assert bench.nvlink_bytes_per_gpu(p, (4, 2), 4) == 2 * (n1 * 2 / 3 + n2)
+    assert bench.remote_fraction((4, 2), 4, 0, 1, ring=True) == 0.0      # rank 1's left neighbour is rank 0
+    assert bench.remote_fraction((4, 2), 4, 0, 2, ring=True) == 1.0      # rank 2's is rank 1 (GPU 0)
     p.close()
 
 

@@ -139,3 +139,79 @@ def test_ideal_time_values():
     t = T.Topology.make((4, 4), (2, 1))
     assert E.ideal_time(S.schedule_collective(t, "RS", 256 * MiB, 4, S.THEMIS)) == 80 * MiB
     assert E.ideal_time(S.schedule_collective(t, "AG", 256 * MiB, 4, S.THEMIS)) == 80 * MiB
+
+
+# ---------------------------------------------------------------- R29: NVLS row
+def test_nvls_fused_pair_bytes_by_message_count():
+    """The fused in-switch RS+AG pair's n = (1 + 1/p) b (R29), counted message
+    by message on the multimem protocol (PAPER.md:493-494 offload): every
+    member m owns piece m (b/p bytes) of the b bytes it holds; for each piece j
+    the switch pulls member m's copy of piece j (ld_reduce on behalf of its
+    owner j) and the owner multicasts the reduced piece once (multimem.st).
+    Sent by member m: its copy of every piece (p x b/p) + one multicast (b/p)."""
+    from oracle import collectives as col
+    for p in (2, 4, 8):
+        b = F(64 * p)
+        piece = b / p
+        sent = [F(0)] * p
+        for j in range(p):                 # piece j, reduced for its owner j
+            for m in range(p):             # the switch reads member m's copy
+                sent[m] += piece
+            sent[j] += piece               # owner j multicasts the sum
+        assert sent == [col.fused_bytes_sent(p, b)] * p
+
+
+def test_nvls_single_dim_closed_form():
+    """D = 1, P = 4, S = 64 B, C = 4, BW 1 B/ns.  Per chunk (16 B): NVLS = one
+    fused op of 16 + 16/4 = 20 ns, its AG half 0 ns -> makespan 4 x 20 = 80 =
+    (5/4) S; the direct algorithm sends 3/4 x 16 = 12 (RS) + 3 x 4 = 12 (AG)
+    per chunk -> 96 = (3/2) S.  P = 2: NVLS 4 x (16 + 8) = 96 = (3/2) S vs
+    direct 4 x (8 + 8) = 64 = S (offload loses at P = 2)."""
+    for p, nv, di in ((4, 80, 96), (2, 96, 64)):
+        for kind, want in ((T.NVLS, nv), (T.DIRECT, di)):
+            t = T.Topology.make((p,), (1,), (kind,))
+            m = E.simulate(S.schedule_collective(t, S.AR, 64, 4, S.THEMIS), E.SCF)
+            assert m.makespan == want
+            assert m.volume == [want]
+
+
+def test_nvls_2x4_tracker_and_timeline():
+    """2x4, dim2 NVLS, BW 1:1 (1 B/ns), S = 16 B, C = 2 (chunk 8 B).
+    Tracker (R1 + R29):
+      c0: loads 0,0 -> baseline (1,2).  RS d1 holds 8: 4 -> L1 = 4; the fused
+          pair on d2 holds 4: 4 + 4/4 = 5 -> L2 = 5; AG d1 holds 4: 4 -> L1 = 8.
+      c1: gap 3 >= thr = 3/4 x 8/16 = 3/8 on m = d2 -> sort (2,1), not fused
+          (last RS dim d1 is direct): RS d2 holds 8: 6; RS d1 holds 2: 1; AG d1
+          holds 1: 1; AG d2 holds 2: 3 x 2 = 6  -> L = [10, 17] = N (B = 1).
+    Timeline (SCF key volume, ready, chunk):
+      t=0  d1: c0s0 [0,4]   d2: c1s0 [0,6]
+      t=6  d1: c1s1 [6,7]   d2: c0s1 fused [6,11]
+      t=7  d1: c1s2 [7,8]   (c1s3 on d2 ready at 8)
+      t=11 d2: ready c1s3 (vol 6, t 8), c0s2 (vol 0, t 11) -> c0s2 [11,11];
+           then d1: c0s3 [11,15]; d2: c1s3 [11,17]      makespan 17
+      busy [10, 17], util 27/34.
+    FIFO (ready, chunk) at t=11 takes c1s3 [11,17], then c0s2 [17,17] and
+    c0s3 [17,21]: makespan 21."""
+    t = T.Topology.make((2, 4), (1, 1), (T.DIRECT, T.NVLS))
+    s = S.schedule_collective(t, S.AR, 16, 2, S.THEMIS)
+    assert [c.rs for c in s.chunks] == [(0, 1), (1, 0)]
+    assert s.loads == [10, 17]
+    assert S.dim_volumes(s) == [10, 17]
+    m = E.simulate(s, E.SCF)
+    assert m.makespan == 17 and m.busy == [10, 17] and m.util == F(27, 34)
+    assert m.start[(0, 1)] == 6 and m.end[(0, 1)] == 11 and m.start[(0, 2)] == 11 and m.end[(0, 2)] == 11
+    assert m.start[(0, 3)] == 11 and m.start[(1, 3)] == 11
+    assert E.simulate(s, E.FIFO).makespan == 21
+
+
+def test_nvls_data_path_is_the_all_reduce():
+    """The fused pair is RS then AG on one dim: the oracle's data executor is
+    unchanged by R29 and still produces the plain All-Reduce (int32 exact)."""
+    from oracle import data as O
+    from synth import host_inputs
+    t = T.Topology.make((2, 4), (1, 1), (T.DIRECT, T.NVLS))
+    xs = host_inputs(8, 8 * 4 * 16, "i32")
+    s = S.schedule_collective(t, S.AR, 8 * 4 * 16 * 4, 4, S.THEMIS)
+    out = O.run_schedule(xs, s, "i32")
+    want = O.allreduce_definition(xs, "i32")
+    assert all((o == want).all() for o in out)

@@ -15,7 +15,7 @@ import pytest
 from oracle import engine as E, scheduler as S, topology as T
 from paper_2110_04478_b200 import themis as th
 
-KINDS = {T.RING: th.RING, T.DIRECT: th.DIRECT, T.SWITCH: th.SWITCH}
+KINDS = {T.RING: th.RING, T.DIRECT: th.DIRECT, T.SWITCH: th.SWITCH, T.NVLS: th.NVLS}
 COLLS = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
 INTRA = {E.SCF: th.SCF, E.FIFO: th.FIFO, E.SCF_LITERAL: th.SCF_LITERAL}
 
@@ -110,8 +110,8 @@ def test_random_configs():
     for _ in range(400):
         D = rng.randint(1, 4)
         sizes = [rng.choice([2, 3, 4, 5, 8, 16]) for _ in range(D)]
-        kinds = [rng.choice([T.RING, T.DIRECT, T.SWITCH]) if s & (s - 1) == 0 else rng.choice([T.RING, T.DIRECT])
-                 for s in sizes]
+        kinds = [rng.choice([T.RING, T.DIRECT, T.SWITCH, T.NVLS]) if s & (s - 1) == 0 else
+                 rng.choice([T.RING, T.DIRECT]) for s in sizes]
         bw = [rng.choice(BWS) if rng.random() < 0.7 else rng.randint(1, 12) for _ in range(D)]
         lat = [rng.choice([0, rng.randint(0, 3000)]) for _ in range(D)]
         o, g = make_pair(sizes, bw, kinds, lat)
@@ -125,6 +125,25 @@ def test_random_configs():
             assert e.status == 4
             skipped += 1
     assert skipped < 40
+
+
+@pytest.mark.parametrize("sizes", [(4,), (8,), (2, 4), (4, 2), (2, 2, 2), (2, 8, 8, 8), (4, 4, 8, 8)])
+def test_nvls_algorithm_row(sizes):
+    """R29: NVLS dims model each AR chunk's last-RS /
+    first-AG pair as one in-switch op; the C++ planner matches the oracle bit
+    for bit (orders, enforced op order, every op time, N_K, tracker), with and
+    without per-op latency, for NVLS on every / some dims."""
+    D = len(sizes)
+    bw = [100000 * (D - k) for k in range(D)]
+    for nv_dims in ({D - 1}, set(range(D))):
+        kinds = [T.NVLS if k in nv_dims else T.SWITCH for k in range(D)]
+        o, g = make_pair(sizes, bw, kinds, [700] * D)
+        for pol in (S.BASELINE, S.THEMIS):
+            for ip in (E.SCF, E.FIFO):
+                compare(o, g, S.AR, 256 << 20, 64, pol, ip)
+            compare(o, g, S.AR, 64 << 20, 16, pol, E.SCF, charge=True)
+        compare(o, g, "RS", 64 << 20, 16, S.THEMIS, E.SCF)          # RS / AG-only: no fused pair
+        compare(o, g, "AG", 64 << 20, 16, S.THEMIS, E.SCF)
 
 
 def test_custom_orders_full_space():
