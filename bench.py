@@ -257,6 +257,32 @@ def run_themis(a):
 
     busbw = lambda t: 2 * S * (P - 1) / P / t / 1e9
 
+    def dim_rates(plan):
+        """Achieved per-dim GB/s per rank of one traced run of `plan`:
+        N_K / busy_K, busy_K = union of dim K's op intervals (%globaltimer);
+        the minimum over GPUs (so every rank plans identically)."""
+        comm.enable_trace(True)
+        refill()
+        th.run(th.ALLREDUCE, comm, plan, N, "f32")
+        torch.cuda.synchronize()
+        comm.status()
+        tr = comm.fetch_trace(plan).astype("int64")
+        comm.enable_trace(False)
+        out = []
+        for k, ops in enumerate(plan.dim_ops()):
+            iv = sorted((int(tr[c, s_, 0]), int(tr[c, s_, 1])) for c, s_ in ops)
+            busy, cs, ce = 0, iv[0][0], iv[0][1]
+            for s0, e0 in iv[1:]:
+                if s0 > ce:
+                    busy += ce - cs
+                    cs, ce = s0, e0
+                else:
+                    ce = max(ce, e0)
+            busy += ce - cs
+            nk = plan.info["dim_volume"][k] / plan.info["byte_scale"]
+            out.append(-max_over_ranks(-(nk / max(busy, 1)), group, dev))
+        return out
+
     main = make(th.THEMIS, ratio)
     # planner cost (SURVEY.md:557): the C++ planner (themis_plan: Algorithm 1 +
     # pre-simulation) for this exact request, median of 21 calls
@@ -297,8 +323,24 @@ def run_themis(a):
                                  "model_makespan_ns": float(p.makespan_ns()), "ctas": p.bound_ctas()}
                     if mode == "paced":   # the paper's utilisation: busBW / sum BW (F2)
                         row[name]["util"] = round(busbw(tt) / sum_bw, 4)
+                    if mode == "caps" and pol == th.BASELINE and len(SIZES) > 1:
+                        # calibrated BW: the per-dim rates this fabric actually
+                        # delivers under these caps (one traced baseline run),
+                        # as the planner's BW_K (B_K from the system)
+                        cal_gbs = dim_rates(p)
                     if not reuse:
                         p.close()
+                if mode == "caps" and len(SIZES) > 1:
+                    cal = tuple(max(1, int(round(r * 1000))) for r in cal_gbs)
+                    pc = th.Plan(th.Topology(SIZES, cal, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF)
+                    check_same_plan(pc, group)
+                    pc.bind(comm, caps_for(rat))
+                    tc_ = timed(pc, max(2, min(a.steps, 5)), 1)[0]
+                    row["themis_calibrated"] = {"bus_gbs": round(busbw(tc_), 1), "ms": round(tc_ * 1e3, 3),
+                                                "calibrated_gbs": [round(r, 1) for r in cal_gbs],
+                                                "greedy_chunks": pc.info["n_greedy"]}
+                    row["calibrated_speedup"] = round(row["baseline"]["ms"] / row["themis_calibrated"]["ms"], 3)
+                    pc.close()
                 row["measured_speedup"] = round(row["baseline"]["ms"] / row["themis"]["ms"], 3)
                 row["model_speedup"] = round(row["baseline"]["model_makespan_ns"] /
                                              row["themis"]["model_makespan_ns"], 4)
@@ -486,6 +528,10 @@ def run_themis(a):
     for key, row in compare.items():
         ent = {"measured_speedup": row["measured_speedup"], "model_speedup": row["model_speedup"],
                "themis_bus_gbs": row["themis"]["bus_gbs"], "baseline_bus_gbs": row["baseline"]["bus_gbs"]}
+        if "themis_calibrated" in row:
+            ent.update(calibrated_speedup=row["calibrated_speedup"],
+                       themis_calibrated_bus_gbs=row["themis_calibrated"]["bus_gbs"],
+                       calibrated_gbs=row["themis_calibrated"]["calibrated_gbs"])
         if "sum_bw_gbs" in row:
             ent.update(sum_bw_gbs=row["sum_bw_gbs"], themis_util=row["themis"]["util"],
                        baseline_util=row["baseline"]["util"],

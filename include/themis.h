@@ -223,8 +223,9 @@ themis_status_t themis_comm_status(themis_comm_t* comm);
  * 16-byte LDG/STG.  Env THEMIS_COPY_ENGINE=ldg|tma sets the default. */
 themis_status_t themis_comm_set_engine(themis_comm_t* comm, int32_t engine);
 /* Bandwidth emulation by pacing (TMA engine): when on, every CTA of dim k's
- * group pulls peer bytes no faster than V * bw_mbps[k] / ctas[k] (absolute
- * due times from a group-shared op origin), so dim k's per-rank rate is capped
+ * group pulls peer bytes no faster than V * bw_mbps[k] / ctas[k] (a per-CTA
+ * leaky bucket over all its units: no credit accrues while it waits for
+ * dependencies), so dim k's per-rank rate is capped
  * at the bound plan topology's absolute bw_mbps[k] (B_K =
  * 1/BW_K); a lone narrow op (op windows without rotation) on w CTAs paces at
  * V * bw_mbps[k] / w per CTA.  Off (default): only the CTA caps limit it. */
@@ -314,6 +315,14 @@ themis_status_t themis_plan_bind(themis_plan_t* plan, themis_comm_t* comm, const
  * Errors: PLAN_MISMATCH if the plan is not bound. */
 themis_status_t themis_plan_launch_hash(const themis_plan_t* plan, uint64_t count, int32_t dtype,
                                         uint64_t* hash /*[host,out]*/);
+/* Debug (single-GPU profiling, fault injection): write into this GPU's local
+ * ranks' signal pads that every logical rank of GPU peer_gpu entered, finished
+ * every op / ring step and exited for all epochs, announcing the launch hash of
+ * (plan, count, dtype).  This GPU's collectives then run alone -- pulling the
+ * peer's heap over NVLink without waiting for it -- so one GPU's kernel can be
+ * profiled (ncu replays it) with real NVLink traffic.  Results are garbage.
+ * Errors: PLAN_MISMATCH (not bound), INVALID_ARG, CUDA. */
+themis_status_t themis_debug_fake_peer_gpu(const themis_plan_t* plan, int32_t peer_gpu, uint64_t count, int32_t dtype);
 /* Number of a bound plan's chunk RS+AG pairs that run as in-switch
  * All-Reduces (NVLS dims on a multicast-capable comm, R29); 0 otherwise.
  * Errors: PLAN_MISMATCH if the plan is not bound. */

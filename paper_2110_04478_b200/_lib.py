@@ -87,6 +87,7 @@ SIGNATURES = {
     "themis_plan_bind": (_ST, [_P, _P, _P]),
     "themis_plan_bound_ctas": (_ST, [_P, _P]),
     "themis_plan_bound_nvls": (_ST, [_P, C.POINTER(C.c_int32)]),
+    "themis_debug_fake_peer_gpu": (_ST, [_P, C.c_int32, C.c_uint64, C.c_int32]),
     "themis_plan_launch_hash": (_ST, [_P, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]),
     "themis_allreduce": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),
     "themis_reduce_scatter": (_ST, [_P, C.c_uint64, C.c_int32, _P, _P]),

@@ -72,7 +72,6 @@ struct themis_comm {
   char* heap[THEMIS_MAX_GPUS] = {};
   uint64_t heap_bytes = 0, vrank_stride = 0, sig_bytes = 0;
   uint32_t* opcnt = nullptr;
-  unsigned long long* op_t0 = nullptr;
   uint32_t* done_cnt = nullptr;
   uint32_t* abort_flag = nullptr;
   uint32_t* epoch_ctr = nullptr;  // device-resident collective epoch (graph-replay safe)
@@ -190,8 +189,6 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
       (e = cudaMalloc(&c->opcnt, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
-      (e = cudaMalloc(&c->op_t0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
-      (e = cudaMemset(c->op_t0, 0, sizeof(unsigned long long) * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->opcnt, 0, sizeof(uint32_t) * (kMaxOps + 8))) != cudaSuccess ||
       (e = cudaMalloc(&c->trace, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
       (e = cudaMemset(c->trace, 0, sizeof(uint64_t) * 8 * kMaxOps)) != cudaSuccess ||
@@ -241,7 +238,6 @@ extern "C" void themis_comm_free(themis_comm_t* c) {
     cudaFree(c->d2h_flags);
   }
   cudaFree(c->opcnt);
-  cudaFree(c->op_t0);
   cudaFree(c->trace);
   cudaFreeHost(c->herr_host);
   delete c;
@@ -506,6 +502,46 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   return THEMIS_OK;
 }
 
+// The plan hash covers the inputs, schedule and per-dim order; mix in the
+// bound CTA caps, the op descriptors' windows and the byte count so every rank
+// must launch identically (checked at kernel entry, R22).
+static uint64_t launch_hash(const themis_plan_t* pl, uint64_t count, int32_t dtype) {
+  uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
+  for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
+  return (h ^ pl->bind->desc_hash) * 1099511628211ull;  // op windows + NVLS rewrite (bind)
+}
+
+// Single-GPU profiling / fault injection: make GPU peer_gpu's logical ranks
+// look as if they had entered, finished every op (and ring step) and exited
+// for every epoch, with this plan's launch hash -- written into the signal pads
+// of this GPU's local ranks.  The kernel on this GPU then never waits, while
+// still pulling the peer's data over NVLink (ncu can replay it: no other GPU
+// takes part).  Data results are meaningless.
+extern "C" themis_status_t themis_debug_fake_peer_gpu(const themis_plan_t* pl, int32_t peer_gpu, uint64_t count,
+                                                      int32_t dtype) {
+  if (!pl || !pl->bind) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan not bound");
+  themis_comm* c = pl->bind->comm;
+  if (peer_gpu < 0 || peer_gpu >= c->W || peer_gpu == c->gpu_rank) return fail(THEMIS_ERR_INVALID_ARG, "bad peer gpu");
+  const int P = c->P, V = c->V;
+  const uint64_t h = launch_hash(pl, count, dtype);
+  std::vector<uint32_t> ones(kMaxOps, 0xFFFFFFFFu);
+  std::vector<unsigned long long> ring(THEMIS_MAX_DIMS * kMaxCtas, ~0ull);
+  for (int v = 0; v < V; ++v) {
+    char* pad = c->heap[c->gpu_rank] + (uint64_t)v * c->sig_bytes;
+    for (int src = peer_gpu * V; src < (peer_gpu + 1) * V; ++src) {
+      const uint32_t m = 0xFFFFFFFFu;
+      CUDA_TRY(cudaMemcpy(pad + 4ull * src, &m, 4, cudaMemcpyHostToDevice));                // entry
+      CUDA_TRY(cudaMemcpy(pad + 4ull * (P + src), &m, 4, cudaMemcpyHostToDevice));          // exit
+      CUDA_TRY(cudaMemcpy(pad + 4ull * (2ull * P + (uint64_t)src * kMaxOps), ones.data(), 4ull * kMaxOps,
+                          cudaMemcpyHostToDevice));                                         // ready
+      CUDA_TRY(cudaMemcpy(pad + ring_flags_offset(P) + 8ull * src * THEMIS_MAX_DIMS * kMaxCtas, ring.data(),
+                          8ull * ring.size(), cudaMemcpyHostToDevice));                    // ring steps
+      CUDA_TRY(cudaMemcpy(pad + hash_offset(P) + 8ull * src, &h, 8, cudaMemcpyHostToDevice));  // plan hash
+    }
+  }
+  return THEMIS_OK;
+}
+
 extern "C" themis_status_t themis_plan_bound_nvls(const themis_plan_t* pl, int32_t* n_pairs) {
   if (!pl || !pl->bind || !n_pairs) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan not bound");
   *n_pairs = pl->bind->nvls_pairs;
@@ -547,14 +583,6 @@ static themis_status_t check_call(int coll, void* buf, uint64_t count, int32_t d
   return THEMIS_OK;
 }
 
-// The plan hash covers the inputs, schedule and per-dim order; mix in the
-// bound CTA caps, the op descriptors' windows and the byte count so every rank
-// must launch identically (checked at kernel entry, R22).
-static uint64_t launch_hash(const themis_plan_t* pl, uint64_t count, int32_t dtype) {
-  uint64_t h = pl->hash ^ (count * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)dtype << 56);
-  for (int k = 0; k < pl->D; ++k) h = (h ^ (uint64_t)pl->bind->ctas[k]) * 1099511628211ull;
-  return (h ^ pl->bind->desc_hash) * 1099511628211ull;  // op windows + NVLS rewrite (bind)
-}
 
 extern "C" themis_status_t themis_plan_launch_hash(const themis_plan_t* pl, uint64_t count, int32_t dtype,
                                                    uint64_t* out) {
@@ -598,7 +626,6 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.elem_size = esz;
   kp.epoch_ctr = c->epoch_ctr;
   kp.opcnt = c->opcnt;
-  kp.op_t0 = c->op_t0;
   kp.done_cnt = c->done_cnt;
   kp.abort_flag = c->abort_flag;
   kp.herr = c->herr_dev;

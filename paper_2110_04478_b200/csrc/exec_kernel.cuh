@@ -56,14 +56,13 @@ struct KParams {
   uint32_t* epoch_ctr;      // device: epoch of the last completed collective on this comm
   unsigned long long plan_hash;  // must be identical on every rank (checked at entry)
   uint32_t* opcnt;          // [kMaxOps] per-op CTA arrival counters
-  unsigned long long* op_t0;  // [kMaxOps] group-wide pacing origin of each op (0 = unset)
   uint32_t* done_cnt;
   uint32_t* abort_flag;     // device-local: someone timed out
   uint32_t* herr;           // host-mapped error word
   uint64_t timeout_ns;
   uint64_t* trace;          // [C*NS*2] or null
   uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
-  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes (0 = off)
+  float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes, leaky bucket (0 = off)
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
   uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
   uint32_t exp;             // experiment bits (env THEMIS_EXP; 0 = the documented protocol)
@@ -347,15 +346,23 @@ static_assert(kThreads == 32 * (kConsumerWarps + 2), "producer + consumers + com
 __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { return ((uint32_t)p.stage_bytes / nsrc) & ~15u; }
 
 // Producer (one lane): stream this CTA's tiles of one unit into the ring.
+__device__ __forceinline__ bool empty_wait(const KParams& p, uint64_t* bar, uint32_t parity) {
+  if (p.exp & 4u) {  // experiment: round 1's plain wait (no abort check)
+    dev::mbar_wait(bar, parity);
+    return true;
+  }
+  return dev::mbar_wait_or(bar, parity, p.abort_flag);
+}
+
 // Returns false if the kernel is aborting (watchdog): every wait for a free
 // ring slot gives up on the abort flag, so a producer whose consumers stopped
 // never spins forever (the CTA then reaches the exit barrier).
 __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
                                              char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
-                                             uint64_t t_op, double& sent) {
+                                             double& due) {
   if (mode == U_NVLS || mode == U_NONE) {  // no TMA: a zero-byte token tells the consumers the deps hold
     const int s = ctr % p.stages;
-    if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) return false;
+    if (!empty_wait(p, &empty[s], ((ctr / p.stages) & 1) ^ 1)) return false;
     dev::mbar_arrive_token(&full[s]);
     ++ctr;
     return true;
@@ -384,13 +391,12 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
         const uint32_t bytes = (uint32_t)(e - pos < big ? e - pos : big);
         for (int j = 0; j < nsrc; ++j, ++ctr) {
           if (pace > 0.f) {
-            const uint64_t due = t_op + (uint64_t)(sent * pace);
-            while (dev::globaltimer() < due) {
+            while ((double)dev::globaltimer() < due) {
             }
-            sent += (double)bytes;
+            due += (double)bytes * pace;
           }
           const int s = ctr % p.stages;
-          if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) {
+          if (!empty_wait(p, &empty[s], ((ctr / p.stages) & 1) ^ 1)) {
             ok = false;
             return;
           }
@@ -405,14 +411,13 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
     }
     for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
       const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
-      if (pace > 0.f) {  // absolute due times from the group's op origin
-        const uint64_t due = t_op + (uint64_t)(sent * pace);
-        while (dev::globaltimer() < due) {
+      if (pace > 0.f) {  // leaky bucket: this CTA's peer bytes at <= 1 / pace bytes/ns
+        while ((double)dev::globaltimer() < due) {
         }
-        sent += (double)bytes * remote;
+        due += (double)bytes * remote * pace;
       }
       const int s = ctr % p.stages;
-      if (!dev::mbar_wait_or(&empty[s], ((ctr / p.stages) & 1) ^ 1, p.abort_flag)) {
+      if (!empty_wait(p, &empty[s], ((ctr / p.stages) & 1) ^ 1)) {
         ok = false;
         return;
       }
@@ -591,10 +596,13 @@ __device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc
   local = __all_sync(0xFFFFFFFFu, local);
   // every storing lane runs the fence (release pattern in its own program
   // order); it is one warp-wide MEMBAR either way
-  if (local)
-    dev::fence_acq_rel_gpu();
-  else
-    dev::fence_acq_rel_sys();
+  if (!(p.exp & 2u) || lane == 0) {
+    if (local)
+      dev::fence_acq_rel_gpu();
+    else
+      dev::fence_acq_rel_sys();
+  }
+  __syncwarp();
   for (int v = lane; v < V; v += 32) {
     const int q = q0 + v;
     dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(cur_epoch(), d.seq, step + 1));
@@ -616,7 +624,6 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
     if (last) {
       if (p.tdetail) p.tdetail[6 * opi + 3] = dev::globaltimer();
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
-      p.op_t0[opi] = 0;
     }
   }
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
@@ -632,10 +639,13 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
     }
     local = __all_sync(0xFFFFFFFFu, local);
     // every storing lane fences (release pattern in its own program order)
-    if (local)
-      dev::fence_acq_rel_gpu();
-    else
-      dev::fence_acq_rel_sys();
+    if (!(p.exp & 2u) || lane == 0) {
+      if (local)
+        dev::fence_acq_rel_gpu();
+      else
+        dev::fence_acq_rel_sys();
+    }
+    __syncwarp();
     if (p.tdetail && lane == 0) p.tdetail[6 * opi + 4] = dev::globaltimer();
     for (int t = lane; t < V * pn; t += 32) {
       const int q = q0 + t / pn;
@@ -743,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
       uint32_t nq = 0;        // units announced
       bool stop = false;
       uint64_t t_wait = 0;
+      double pace_due = 0.0;  // lane 0: pacing bucket (ns)
       while (!stop) {
         while (head < nops) {  // drop taken / foreign ops at the head
           int li, wn;
@@ -789,13 +800,11 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         int li, wn;
         op_member(d, gi, gn, li, wn);
         const bool work = unit_has_work(p, d, mode, li, wn);
-        uint64_t t_op = 0;
-        double sent = 0.0;
         for (int u = 0; u < nu && !stop; ++u, ++nq) {
           const int slot = nq % kOpRing;
           bool w = true;
           if (lane == 0) {  // announce the unit once the followers released the queue slot
-            w = dev::mbar_wait_or(&op_free[slot], ((nq / kOpRing) & 1) ^ 1, p.abort_flag);
+            w = (p.exp & 8u) ? true : dev::mbar_wait_or(&op_free[slot], ((nq / kOpRing) & 1) ^ 1, p.abort_flag);
             if (w) {
               s_q[slot] = opi * 64 + u;
               dev::mbar_arrive(&q_full[slot]);
@@ -821,13 +830,14 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
                 dev::fence_proxy_async_global();
                 p.tdetail[6 * opi + 5] = dev::globaltimer();
               }
-              if (p.pace_ns_per_byte[d.dim] > 0.f) {  // group-shared pacing origin (first starter wins)
-                const unsigned long long now = dev::globaltimer();
-                const unsigned long long prev = atomicCAS(&p.op_t0[opi], 0ull, now);
-                t_op = prev ? prev : now;
-              }
             }
-            if (!produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, t_op, sent)) stop = true;
+            // pacing (BW emulation): a per-CTA leaky bucket across all the
+            // CTA's units -- no credit accrues while it waits for a unit's
+            // dependencies, so a dim's c_k CTAs never exceed V * BW_k in total,
+            // whatever order (or how many ops at once) they run
+            const double now = (double)dev::globaltimer();
+            if (pace_due < now) pace_due = now;
+            if (!produce_unit(p, d, mode, u, li, wn, smem, full, empty, ctr, pace_due)) stop = true;
             if (p.tdetail && li == 0 && u + 1 == nu) p.tdetail[6 * opi + 0] = dev::globaltimer();
           }
           stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
