@@ -347,10 +347,6 @@ __device__ __forceinline__ uint32_t unit_tile(const KParams& p, int nsrc) { retu
 
 // Producer (one lane): stream this CTA's tiles of one unit into the ring.
 __device__ __forceinline__ bool empty_wait(const KParams& p, uint64_t* bar, uint32_t parity) {
-  if (p.exp & 4u) {  // experiment: round 1's plain wait (no abort check)
-    dev::mbar_wait(bar, parity);
-    return true;
-  }
   return dev::mbar_wait_or(bar, parity, p.abort_flag);
 }
 
@@ -434,16 +430,10 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
   return ok;
 }
 
-// Hand a ring slot back to the producer after this warp's reads of it.
-// Default: a release arrive (the reads happen-before the producer's acquire and
-// its next TMA write into the slot).  Experiment bit 0 (THEMIS_EXP=1): relaxed
-// arrive (the reads' values were already consumed by the stores before it).
-__device__ __forceinline__ void slot_release(const KParams& p, uint64_t* bar) {
-  if (p.exp & 1u)
-    dev::mbar_arrive_relaxed(bar);
-  else
-    dev::mbar_arrive(bar);
-}
+// Hand a ring slot back to the producer after this warp's reads of it: a
+// release arrive (the reads happen-before the producer's acquire and its next
+// TMA write into the slot; measured: no cost over a relaxed arrive).
+__device__ __forceinline__ void slot_release(const KParams&, uint64_t* bar) { dev::mbar_arrive(bar); }
 
 // Consumers: returns false if the kernel is aborting (watchdog).
 template <class Tag>
@@ -571,6 +561,8 @@ __device__ __forceinline__ bool deps_ready_warp(const KParams& p, const OpDesc& 
   return __all_sync(0xFFFFFFFFu, ok);
 }
 
+constexpr int kFewFlags = 16;  // flag stores a single lane issues after its one release fence
+
 __device__ __forceinline__ unsigned long long ring_flag_value(uint32_t epoch, int seq, int steps_done) {
   return ((unsigned long long)epoch << 32) | ((unsigned long long)seq << 8) | (unsigned long long)steps_done;
 }
@@ -594,18 +586,29 @@ __device__ __forceinline__ void publish_ring_warp(const KParams& p, const OpDesc
   bool local = true;
   for (int v = lane; v < V; v += 32) local &= ring_peer(p, q0 + v, k, +1) / V == p.my_gpu;
   local = __all_sync(0xFFFFFFFFu, local);
-  // every storing lane runs the fence (release pattern in its own program
-  // order); it is one warp-wide MEMBAR either way
-  if (!(p.exp & 2u) || lane == 0) {
+  // release pattern: a fence then relaxed flag stores in the same thread's
+  // program order.  A fence on every lane of the warp costs ~10 % of NVLink
+  // throughput (fence.acq_rel.sys is per thread), so few flags are stored by
+  // lane 0 alone after its one fence.
+  if (V <= kFewFlags) {
+    if (lane == 0) {
+      if (local)
+        dev::fence_acq_rel_gpu();
+      else
+        dev::fence_acq_rel_sys();
+      for (int v = 0; v < V; ++v)
+        dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q0 + v, k, +1), q0 + v, k, gi),
+                              ring_flag_value(cur_epoch(), d.seq, step + 1));
+    }
+  } else {
     if (local)
       dev::fence_acq_rel_gpu();
     else
       dev::fence_acq_rel_sys();
-  }
-  __syncwarp();
-  for (int v = lane; v < V; v += 32) {
-    const int q = q0 + v;
-    dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(cur_epoch(), d.seq, step + 1));
+    for (int v = lane; v < V; v += 32) {
+      const int q = q0 + v;
+      dev::st_relaxed_sys64(ring_slot(p, ring_peer(p, q, k, +1), q, k, gi), ring_flag_value(cur_epoch(), d.seq, step + 1));
+    }
   }
   __syncwarp();
 }
@@ -638,22 +641,33 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
       local &= (q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn]) / V == p.my_gpu;
     }
     local = __all_sync(0xFFFFFFFFu, local);
-    // every storing lane fences (release pattern in its own program order)
-    if (!(p.exp & 2u) || lane == 0) {
-      if (local)
-        dev::fence_acq_rel_gpu();
-      else
-        dev::fence_acq_rel_sys();
-    }
-    __syncwarp();
-    if (p.tdetail && lane == 0) p.tdetail[6 * opi + 4] = dev::globaltimer();
-    for (int t = lane; t < V * pn; t += 32) {
+    // release pattern (fence, then relaxed flag stores in the same thread's
+    // program order); few flags: lane 0 alone, after one fence
+    const int nst = V * pn;
+    auto publish = [&](int t) {
       const int q = q0 + t / pn;
       const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
       if (local)
         dev::st_relaxed_gpu(ready_slot(p, dst, q, opi), cur_epoch());
       else
         dev::st_relaxed_sys(ready_slot(p, dst, q, opi), cur_epoch());
+    };
+    if (nst <= kFewFlags) {
+      if (lane == 0) {
+        if (local)
+          dev::fence_acq_rel_gpu();
+        else
+          dev::fence_acq_rel_sys();
+        if (p.tdetail) p.tdetail[6 * opi + 4] = dev::globaltimer();
+        for (int t = 0; t < nst; ++t) publish(t);
+      }
+    } else {
+      if (local)
+        dev::fence_acq_rel_gpu();
+      else
+        dev::fence_acq_rel_sys();
+      if (p.tdetail && lane == 0) p.tdetail[6 * opi + 4] = dev::globaltimer();
+      for (int t = lane; t < nst; t += 32) publish(t);
     }
   }
   else if (p.host_seq && lane == 0) {  // last stage: chunk c is final here -> the D2H stream may copy it
@@ -804,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
           const int slot = nq % kOpRing;
           bool w = true;
           if (lane == 0) {  // announce the unit once the followers released the queue slot
-            w = (p.exp & 8u) ? true : dev::mbar_wait_or(&op_free[slot], ((nq / kOpRing) & 1) ^ 1, p.abort_flag);
+            w = dev::mbar_wait_or(&op_free[slot], ((nq / kOpRing) & 1) ^ 1, p.abort_flag);
             if (w) {
               s_q[slot] = opi * 64 + u;
               dev::mbar_arrive(&q_full[slot]);

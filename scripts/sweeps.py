@@ -36,6 +36,7 @@ from synth import WORKLOAD_PARAMS, bucket_sizes, device_input, torch_dtype  # no
 import bench  # noqa: E402
 
 CONC = 1
+LA = 1        # --lookahead: runtime intra-dim order (R28)
 LAT = 0       # --latency-ns: measured per-op A_K for the latency-aware auto-chunk column (config 3)
 
 
@@ -49,6 +50,7 @@ class Runner:
         topo = th.Topology(tuple(sizes), (1,) * len(sizes))
         c = th.Comm(topo, max_bytes, group=self.group, device=self.local)
         c.set_timeout(30.0)
+        c.set_lookahead(LA)
         lay = bench.logical_layout(sizes, self.world)
         ncross = len(lay["cross_gpu_dims"])
         c.set_stages(6 if ncross < len(sizes) else (2 if len(sizes) > 1 else 4))
@@ -76,6 +78,27 @@ class Runner:
         comm.status()
         return max_over_ranks(sum(ts) / len(ts), self.group, self.dev)
 
+    def nccl_bus_gbs(self, nbytes, dtype="f32", steps=5):
+        """Context row: torch.distributed.all_reduce (NCCL) of nbytes per GPU,
+        flat over the W GPUs, bus GB/s (max over GPUs of the mean time)."""
+        if self.world == 1:
+            return None
+        import torch.distributed as dist
+        x = torch.ones(nbytes // (2 if dtype == "bf16" else 4), device=self.dev,
+                       dtype=torch.bfloat16 if dtype == "bf16" else torch.float32)
+        for _ in range(2):
+            dist.all_reduce(x, group=self.group)
+        barrier(self.group, self.dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            dist.all_reduce(x, group=self.group)
+        e1.record()
+        torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1) / 1e3 / steps, self.group, self.dev)
+        return round(2 * nbytes * (self.world - 1) / self.world / t / 1e9, 2)
+
     def emit(self, row):
         if self.rank == 0:
             print(json.dumps(row), flush=True)
@@ -99,6 +122,9 @@ def config3(r: Runner, quick):
         ratios = [(1,) * len(sizes)] + ([(200, 50)] if len(sizes) == 2 else [])
         pace_total = 240.0 if r.V > 1 else 500.0
         for S_mib in sizes_mib:
+            if r.world > 1:   # NCCL context row for this size (flat, same bytes per GPU)
+                r.emit({"config": 3, "n_gpus": W, "topology": "nccl-flat", "mib": S_mib,
+                        "nccl_bus_gbs": r.nccl_bus_gbs(S_mib << 20)})
             for C in chunks:
                 S = S_mib << 20
                 if (S // 4) % (P * C * 4):
@@ -150,6 +176,11 @@ def config4(r: Runner, quick):
             buckets = buckets[:3] + buckets[-1:]
         maxc = pad_count(max(buckets), P, th.AUTO_MAX_CHUNKS, 2)     # room for every chunk-count candidate
         comm = r.comm(sizes, maxc * 2)
+        if r.world > 1:   # NCCL context: the same bf16 bucket trace through torch.distributed.all_reduce
+            per = [r.nccl_bus_gbs(pad_count(n, P, C, 2) * 2, "bf16") for n in buckets]
+            tot = sum(2 * pad_count(n, P, C, 2) * 2 * (r.world - 1) / r.world / (g * 1e9) for n, g in zip(buckets, per))
+            r.emit({"config": 4, "n_gpus": r.world, "model": model, "mode": "nccl-flat", "bucket_bus_gbs": per,
+                    "total_ms": round(tot * 1e3, 3)})
         for rat in [(1, 1, 1), (4, 2, 1)]:
             for mode in ("caps", "paced"):
                 comm.set_pacing(mode == "paced")
@@ -223,14 +254,16 @@ def main():
     ap.add_argument("--config", type=int, required=True, choices=[3, 4, 5])
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--concurrency", type=int, default=1, help="ops in flight per dim (plans)")
+    ap.add_argument("--lookahead", type=int, default=1, help="runtime intra-dim order window (R28)")
     ap.add_argument("--latency-ns", type=int, default=0,
                     help="config 3: also time a latency-aware Themis plan with planner-chosen chunks (A_K ns)")
     a = ap.parse_args()
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     torch.cuda.set_device(local)
-    global CONC, LAT
+    global CONC, LAT, LA
     CONC = a.concurrency
+    LA = a.lookahead
     LAT = a.latency_ns
     r = Runner(group, rank, world, local)
     {3: config3, 4: config4, 5: config5}[a.config](r, a.quick)
