@@ -331,10 +331,20 @@ def run_themis(a):
                     if not reuse:
                         p.close()
                 if mode == "caps" and len(SIZES) > 1:
-                    cal = tuple(max(1, int(round(r * 1000))) for r in cal_gbs)
-                    pc = th.Plan(th.Topology(SIZES, cal, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF)
-                    check_same_plan(pc, group)
-                    pc.bind(comm, caps_for(rat))
+                    # quantised to 1/32 of the fastest dim's rate (keeps lcm(BW) -- the
+                    # planner's exact time scale -- small; R21)
+                    def cal_plan(rates):
+                        q = max(1.0, max(rates) / 32)
+                        cal = tuple(max(1, int(round(r / q))) * int(round(q * 1000)) for r in rates)
+                        pc_ = th.Plan(th.Topology(SIZES, cal, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF)
+                        check_same_plan(pc_, group)
+                        return pc_.bind(comm, caps_for(rat))
+                    # a dim delivers at least the best rate it showed in any run:
+                    # one refinement with the calibrated plan's own rates
+                    pc = cal_plan(cal_gbs)
+                    cal_gbs = [max(x, y) for x, y in zip(cal_gbs, dim_rates(pc))]
+                    pc.close()
+                    pc = cal_plan(cal_gbs)
                     tc_ = timed(pc, max(2, min(a.steps, 5)), 1)[0]
                     row["themis_calibrated"] = {"bus_gbs": round(busbw(tc_), 1), "ms": round(tc_ * 1e3, 3),
                                                 "calibrated_gbs": [round(r, 1) for r in cal_gbs],

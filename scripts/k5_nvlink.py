@@ -62,6 +62,9 @@ def main():
     ap.add_argument("--stage-kb", type=int, default=32)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--all-gpus", action="store_true",
+                    help="every GPU runs its rank alone at once (all peers faked): bidirectional NVLink "
+                         "traffic with no cross-GPU waits -- the executor's ceiling without dependencies")
     a = ap.parse_args()
     S = a.mib << 20
     N = S // 4
@@ -71,58 +74,78 @@ def main():
     topo = th.Topology(sizes, tuple(int(b * 1000) for b in bw))
     P = topo.P
     sig, stride, hb = th.heap_layout(P, P, S)
-    heaps = [0] * P
-    for g in range(1, P):
-        enable_peer(0, g)
+    for g in range(P):
+        for h in range(P):
+            if h != g:
+                enable_peer(g, h)
+    runners = list(range(P)) if a.all_gpus else [0]
+    # runner g's view: its own heap on GPU g, and for every other GPU h a heap
+    # of its own on GPU h (pulled over NVLink; g's flag writes land there, so
+    # runners never see each other's flags and none ever waits)
+    allocs = []
+
+    def alloc(dev_):
+        torch.cuda.set_device(dev_)
+        h_ = C.c_void_p()
+        check(lib().themis_heap_alloc(hb, C.byref(h_)))
+        allocs.append((dev_, h_.value))
+        return h_.value
+
+    view = {g: [alloc(h) for h in range(P)] for g in runners}
+    comms, plans, streams = {}, {}, {}
+    for g in runners:
         torch.cuda.set_device(g)
-        h = C.c_void_p()
-        check(lib().themis_heap_alloc(hb, C.byref(h)))
-        heaps[g] = h.value
-    torch.cuda.set_device(0)
-    h0 = C.c_void_p()
-    check(lib().themis_heap_alloc(hb, C.byref(h0)))
-    heaps[0] = h0.value
-    comm = C.c_void_p()
-    tc = topo.to_c()
-    check(lib().themis_comm_create(0, P, C.byref(tc), (C.c_void_p * MAX_GPUS)(*heaps), hb, stride, C.byref(comm)))
-    check(lib().themis_comm_set_stages(comm, 1))
-    check(lib().themis_comm_set_stage_bytes(comm, a.stage_kb * 1024))
-    check(lib().themis_comm_set_stages(comm, a.stages))
-    check(lib().themis_comm_set_pacing(comm, int(a.paced)))
-    check(lib().themis_comm_set_lookahead(comm, a.lookahead))
-    plan = th.Plan(topo, th.ALLREDUCE, S, a.chunks)
-    arr = (C.c_int32 * MAX_GPUS)(*ctas)
-    check(lib().themis_plan_bind(plan.h, comm, arr))
-    for g in range(1, P):
-        check(lib().themis_debug_fake_peer_gpu(plan.h, g, N, 0))
-    buf = h0.value + sig
-    stream = torch.cuda.current_stream()
+        comm = C.c_void_p()
+        tc = topo.to_c()
+        check(lib().themis_comm_create(g, P, C.byref(tc), (C.c_void_p * MAX_GPUS)(*view[g]), hb, stride,
+                                       C.byref(comm)))
+        check(lib().themis_comm_set_stages(comm, 1))
+        check(lib().themis_comm_set_stage_bytes(comm, a.stage_kb * 1024))
+        check(lib().themis_comm_set_stages(comm, a.stages))
+        check(lib().themis_comm_set_pacing(comm, int(a.paced)))
+        check(lib().themis_comm_set_lookahead(comm, a.lookahead))
+        plan = th.Plan(topo, th.ALLREDUCE, S, a.chunks)
+        arr = (C.c_int32 * MAX_GPUS)(*ctas)
+        check(lib().themis_plan_bind(plan.h, comm, arr))
+        for h in range(P):
+            if h != g:
+                check(lib().themis_debug_fake_peer_gpu(plan.h, h, N, 0))
+        comms[g], plans[g], streams[g] = comm, plan, torch.cuda.current_stream(g)
     ts = []
     for i in range(a.iters + 2):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        check(lib().themis_allreduce(buf, N, 0, plan.h, stream.cuda_stream))
-        e1.record()
-        torch.cuda.synchronize()
-        check(lib().themis_comm_status(comm))
+        ev = {}
+        for g in runners:
+            torch.cuda.set_device(g)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(streams[g])
+            check(lib().themis_allreduce(view[g][g] + sig, N, 0, plans[g].h, streams[g].cuda_stream))
+            e1.record(streams[g])
+            ev[g] = (e0, e1)
+        for g in runners:
+            torch.cuda.set_device(g)
+            torch.cuda.synchronize(g)
+            check(lib().themis_comm_status(comms[g]))
         if i >= 2:
-            ts.append(e0.elapsed_time(e1) / 1e3)
+            ts.append(max(ev[g][0].elapsed_time(ev[g][1]) / 1e3 for g in runners))
     t = sum(ts) / len(ts)
+    plan = plans[0]
     # one rank per GPU: every pulled byte crosses NVLink, sum_K N_K = 2 S (P-1)/P (F2)
     vol = [v / plan.info["byte_scale"] for v in plan.info["dim_volume"]]
     nvlink_bytes = sum(vol)
     out = {"tag": a.tag, "sizes": list(sizes), "mib": a.mib, "chunks": a.chunks, "ctas": ctas, "paced": a.paced,
            "emulated_gbs": bw, "stages": a.stages, "stage_kb": a.stage_kb, "lookahead": a.lookahead,
+           "all_gpus": a.all_gpus,
            "ms": round(t * 1e3, 4), "nvlink_bytes": nvlink_bytes, "bus_gbs": round(nvlink_bytes / t / 1e9, 2)}
     if len(sizes) == 1:
         out["ratio_to_emulated"] = round(nvlink_bytes / t / 1e9 / bw[0], 4)
     print(json.dumps(out), flush=True)
-    plan.close()
-    lib().themis_comm_free(comm)
-    lib().themis_heap_free(h0)
-    for g in range(1, P):
+    for g in runners:
         torch.cuda.set_device(g)
-        lib().themis_heap_free(C.c_void_p(heaps[g]))
+        plans[g].close()
+        lib().themis_comm_free(comms[g])
+    for dev_, h_ in allocs:
+        torch.cuda.set_device(dev_)
+        lib().themis_heap_free(C.c_void_p(h_))
 
 
 if __name__ == "__main__":
