@@ -305,9 +305,12 @@ def run_themis(a):
     ncross = len(lay["cross_gpu_dims"])
     # ~80% of the physical limits, so the emulated BW (not the fabric) binds
     # even when Themis keeps every dimension busy at once.
-    caps_ = [500.0, 0.8 * 6000.0 / (2.5 * V)]
+    # NVLink: ~640 GB/s per GPU is the executor's bidirectional ceiling
+    # (profiles/r02/ceilings: all GPUs pulling at once, no dependencies), so
+    # ~600 per GPU over the cross-GPU dims' share keeps the emulated BW binding
+    caps_ = [600.0, 0.8 * 6000.0 / (2.5 * V)]
     if ncross:
-        caps_.append(500.0 * len(SIZES) / (V * ncross))
+        caps_.append(600.0 * len(SIZES) / (V * ncross))
     pace_gbs = a.pace_gbs or float(int(min(caps_) // 24) * 24)
     if not a.no_compare:
         for mode in ("caps", "paced"):
@@ -695,7 +698,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
     ap.add_argument("--stage-kb", type=int, default=0, help="TMA ring stage size (KiB; default by topology)")
-    ap.add_argument("--lookahead", type=int, default=1,
+    ap.add_argument("--lookahead", type=int, default=16,
                     help="runtime intra-dim order: 1 = enforced pre-simulated order, L > 1 = first ready of the next L (R28)")
     ap.add_argument("--concurrency", type=int, default=1,
                     help="ops in flight per dimension in the plan's pre-simulation (1 = the paper's model)")
