@@ -416,7 +416,7 @@ def run_themis(a):
 
     # NCCL all_reduce on the same bytes (context row, N > 1 only)
     nccl = None
-    if world > 1 and not a.no_compare:
+    if world > 1 and (not a.no_compare or a.nccl):
         import torch.distributed as dist
         x = pristine[0].clone()
         for _ in range(2):
@@ -694,6 +694,7 @@ def main():
     ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")
     ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
     ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--nccl", action="store_true", help="NCCL context row even with --no-compare")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
