@@ -251,6 +251,17 @@ themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t byte
  * small op occupies (and synchronises) only the CTAs it needs.  Takes effect at
  * the next themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rotate);
+/* Push-mode All-Gather (DESIGN R30): on = 1 (env THEMIS_PUSH), at the next
+ * themis_plan_bind every direct-algorithm AG op (not ring, not NVLS) runs by
+ * WRITES: each rank streams its own held part through shared memory and TMA
+ * bulk-stores it into its P_k - 1 dim peers' buffers (NVLink carries data in
+ * write requests instead of read responses + read requests), and the chunk's
+ * next stage waits for the whole k x k' plane of ranks that wrote into its
+ * sources.  Same results bit for bit (AG copies).  All ranks must bind with
+ * the same setting (part of the launch hash).  Host-buffer streaming
+ * (themis_allreduce_host) and the LDG engine run AG ops as pulls.
+ * Errors: INVALID_ARG. */
+themis_status_t themis_comm_set_push(themis_comm_t* comm, int32_t on);
 /* Runtime intra-dimension order (DESIGN R28).  lookahead = 1
  * (default, env THEMIS_LOOKAHEAD): every dimension group runs its ops in the
  * pre-simulated enforced order.  L in 2..32: on dims that

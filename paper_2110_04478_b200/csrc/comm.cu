@@ -87,6 +87,7 @@ struct themis_comm {
   int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
   int lookahead = 1;           // runtime intra-dim order window (themis_comm_set_lookahead); 1 = static
   uint32_t exp = 0;            // experiment bits (env THEMIS_EXP)
+  int push_ag = 0;             // direct AG ops as pushes (themis_comm_set_push, R30); applies at bind
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -216,6 +217,7 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
     c->stages = std::max(1, std::min(std::min(kStages, kStages * kStageBytes / c->stage_bytes), atoi(env)));
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   if (const char* env = getenv("THEMIS_WINDOW_ROTATE")) c->window_rotate = atoi(env) != 0;
+  if (const char* env = getenv("THEMIS_PUSH")) c->push_ag = atoi(env) != 0;
   if (const char* env = getenv("THEMIS_EXP")) c->exp = (uint32_t)strtoul(env, nullptr, 0);
   if (const char* env = getenv("THEMIS_LOOKAHEAD")) c->lookahead = std::max(1, std::min(kMaxLookahead, atoi(env)));
   c->max_blocks = nb * c->num_sms;
@@ -265,6 +267,11 @@ extern "C" themis_status_t themis_comm_set_multicast(themis_comm_t* c, void* mc_
 extern "C" themis_status_t themis_comm_set_window_rotation(themis_comm_t* c, int32_t rotate) {
   if (!c || rotate < 0 || rotate > 1) return fail(THEMIS_ERR_INVALID_ARG, "rotate must be 0 or 1");
   c->window_rotate = rotate;
+  return THEMIS_OK;
+}
+extern "C" themis_status_t themis_comm_set_push(themis_comm_t* c, int32_t on) {
+  if (!c || on < 0 || on > 1) return fail(THEMIS_ERR_INVALID_ARG, "push must be 0 or 1");
+  c->push_ag = on;
   return THEMIS_OK;
 }
 extern "C" themis_status_t themis_comm_set_lookahead(themis_comm_t* c, int32_t lookahead) {
@@ -410,6 +417,13 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
         }
       }
   }
+  // R30: direct (non-ring, non-NVLS) AG ops as pushes; the op after a push
+  // waits for the push's k x k' plane
+  for (size_t i = 0; i < ops.size(); ++i) {
+    ops[i].prev_dim = ops[i].stage > 0 ? ops[i - 1].dim : -1;
+    ops[i].push = c->push_ag && ops[i].phase == 1 && !ops[i].ring && !ops[i].nvls;
+  }
+  for (size_t i = 0; i < ops.size(); ++i) ops[i].prev_push = ops[i].stage > 0 && ops[i - 1].push;
   std::vector<int32_t> lists((size_t)D * pl->C * pl->NS, 0);
   for (int k = 0; k < D; ++k)
     for (size_t i = 0; i < pl->dim_ops[k].size(); ++i) {
@@ -469,6 +483,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     mix(d.ring);
     mix(d.nvls);
     mix(d.seq);
+    mix(d.push);
     uint32_t ps;
     std::memcpy(&ps, &d.pace_scale, 4);
     mix(ps);
@@ -634,6 +649,7 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   kp.plan_hash = launch_hash(pl, count, dtype);
   kp.lookahead = c->lookahead;
+  kp.push_ok = c->engine && !host_seq;  // host streaming publishes per-chunk d2h flags from the last stage: pull
   kp.exp = c->exp;
   kp.dyn_mask = pl->bind->dyn_mask;
   kp.stages = c->stages;

@@ -21,7 +21,8 @@
 constexpr int kMaxCtas = 160;  // CTAs per dimension group (ring step flags)
 enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3, U_DIRECT_AG_T = 4,
                 U_NVLS = 5,   // fused NVLS All-Reduce of the own piece on a switch dim (RS op of an RS+AG pair)
-                U_NONE = 6 }; // its AG partner: no data (the NVLS broadcast delivered it), dependencies only
+                U_NONE = 6,   // its AG partner: no data (the NVLS broadcast delivered it), dependencies only
+                U_PUSH_AG = 7 };  // direct AG by writes: the own held part -> every dim peer (TMA bulk stores, R30)
 
 // Per-op descriptor uploaded at bind (a5).
 struct OpDesc {
@@ -30,6 +31,9 @@ struct OpDesc {
   int32_t next_dim;                  // dim of stage+1 (-1: last stage)
   int32_t ring;                      // 1: ring algorithm on this dim
   int32_t nvls;                      // 1: U_NVLS (fused RS+AG through the switch), 2: U_NONE (its AG partner)
+  int32_t push;                      // 1: direct AG executed as pushes (U_PUSH_AG, R30)
+  int32_t prev_push;                 // the chunk's previous stage was a push: wait for its k x k' plane (R30)
+  int32_t prev_dim;                  // dim of stage - 1 (-1: first stage)
   int32_t seq;                       // index of the op in its dim's enforced list
   int32_t width, offset;             // the op runs on CTAs [offset, offset+width) mod c_k of its group
   float pace_scale;                  // pacing: width / c_k for a lone narrow op (it gets the whole dim rate), else 1
@@ -66,6 +70,7 @@ struct KParams {
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
   uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
   uint32_t exp;             // experiment bits (env THEMIS_EXP; 0 = the documented protocol)
+  int32_t push_ok;          // push AG allowed in this launch (off while host-buffer streaming)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
@@ -183,8 +188,10 @@ __device__ __forceinline__ int unit_mode(const OpDesc& d) {
 }
 // TMA path: a direct AG tile pulls the same offsets from all P_k - 1 peers at
 // once (U_DIRECT_AG_T), so every CTA keeps requests in flight to every peer.
-__device__ __forceinline__ int unit_mode_tma(const OpDesc& d) {
+__device__ __forceinline__ bool is_push(const KParams& p, const OpDesc& d) { return d.push && p.push_ok; }
+__device__ __forceinline__ int unit_mode_tma(const KParams& p, const OpDesc& d) {
   if (d.nvls) return d.nvls == 1 ? U_NVLS : U_NONE;
+  if (is_push(p, d)) return U_PUSH_AG;
   const int m = unit_mode(d);
   return m == U_DIRECT_AG ? U_DIRECT_AG_T : m;
 }
@@ -222,7 +229,7 @@ __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, i
     f = it - vq * nblk;
     r.j = -1;
     const int ck = coord(p, r.q, k);
-    digit = (mode == U_DIRECT_RS || mode == U_NVLS) ? ck
+    digit = (mode == U_DIRECT_RS || mode == U_NVLS || mode == U_PUSH_AG) ? ck
           : mode == U_DIRECT_AG_T ? 0  // base: part j is at off + j * part_stride
           : mode == U_RING_RS     ? (ck + pk - 2 - step) % pk
                                   : ((ck - 1 - step) % pk + pk) % pk;
@@ -290,6 +297,7 @@ __device__ __forceinline__ int unit_src_rank(const KParams& p, const OpDesc& d, 
     case U_DIRECT_AG: return m.g0 + m.j * (int)p.stride[k];
     case U_DIRECT_AG_T: return m.g0 + peer_member(j, coord(p, m.q, k)) * (int)p.stride[k];
     case U_RING_RS: return j == 0 ? ring_peer(p, m.q, k, -1) : m.q;  // left partial + own value
+    case U_PUSH_AG: return m.q;                                      // the own held part
     default: return ring_peer(p, m.q, k, -1);
   }
 }
@@ -367,7 +375,8 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
   const int nsrc = unit_nsrc(p, d, mode);
   const uint32_t tile = unit_tile(p, nsrc);
   const float pace = p.pace_ns_per_byte[d.dim] * d.pace_scale;
-  const int remote = (mode == U_DIRECT_RS || mode == U_DIRECT_AG_T) ? p.size[d.dim] - 1 : 1;  // peer sources/tile
+  const int remote = (mode == U_DIRECT_RS || mode == U_DIRECT_AG_T || mode == U_PUSH_AG) ? p.size[d.dim] - 1
+                                                                                          : 1;  // peer bytes / tile byte
   const uint64_t pstride = part_stride(p, d.dim);
   dev::fence_proxy_async_global();  // generic-proxy writes (ours and peers') -> async proxy (TMA)
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
@@ -471,6 +480,55 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
     ++ctr;
     return true;
   }
+  if (mode == U_PUSH_AG) {
+    // R30: consumer thread 0 writes every landed tile of the own held part to
+    // the P_k - 1 dim peers (TMA bulk stores, same offsets in their buffers),
+    // one bulk group per tile, pipelined: a tile's slot is released (by warp
+    // 1) once the NEXT tile's stores are issued and this tile's stores have
+    // read it (wait_group.read 1); the other consumer warps release at once.
+    // The unit ends only when every store's writes are complete (then
+    // op_done -> the completion warp's release publish).
+    const int pk = p.size[d.dim];
+    int held = -1;  // warp 1: slot whose stores may still be reading it
+    for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+      if (!ok) return;
+      const Item m = decode_item(p, d, mode, step, it);
+      const int ck = coord(p, m.q, d.dim);
+      for (uint64_t pos = a; pos < e; pos += tile, ++ctr) {
+        const uint32_t bytes = (uint32_t)(e - pos < tile ? e - pos : tile);
+        const int s = ctr % p.stages;
+        if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) {
+          ok = false;
+          return;
+        }
+        if (ct < 32) {
+          if (ct == 0) {
+            for (int j = 0; j < pk; ++j)
+              if (j != ck)
+                dev::bulk_s2g(data_of(p, m.g0 + j * (int)p.stride[d.dim]) + m.off + pos, smem + s * p.stage_bytes,
+                              bytes);
+            dev::bulk_commit();
+            dev::bulk_wait_read1();
+          }
+          __syncwarp();
+          if (held >= 0 && lane == 0) slot_release(p, &empty[held]);
+          held = s;
+        } else {
+          __syncwarp();
+          if (lane == 0) slot_release(p, &empty[s]);
+        }
+      }
+    });
+    if (ct < 32) {
+      if (ct == 0) {
+        dev::bulk_wait0();                 // writes performed ...
+        dev::fence_proxy_async_global();   // ... and ordered before the generic-proxy release chain
+      }
+      __syncwarp();
+      if (held >= 0 && lane == 0) slot_release(p, &empty[held]);
+    }
+    return ok;
+  }
   for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
     if (!ok) return;
     const Item m = decode_item(p, d, mode, step, it);
@@ -529,15 +587,29 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
   return ok;
 }
 
+// Sources whose (c, s-1) flag an op of local rank q waits for: q's dim-k
+// group (P_k ranks) -- or, after a push stage on dim k' (R30), the whole
+// k' x k plane through q (P_k' x P_k ranks: q's dim-k peers read data that
+// their dim-k' peers wrote into them).
+__device__ __forceinline__ int n_deps(const KParams& p, const OpDesc& d) {
+  return p.size[d.dim] * ((d.prev_push && p.push_ok) ? p.size[d.prev_dim] : 1);
+}
+__device__ __forceinline__ int dep_src(const KParams& p, const OpDesc& d, int q, int t) {
+  const int k = d.dim, pk = p.size[k];
+  int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+  if (d.prev_push && p.push_ok) src += (t / pk - coord(p, q, d.prev_dim)) * (int)p.stride[d.prev_dim];
+  return src;
+}
+
 // One warp: wait until the local ranks and their dim-k peers completed (c, s-1).
 // Stage s > 0: every source finished (c, s-1).  Stage 0 in host-buffer mode:
 // every source GPU's copy of chunk c has landed (h2d flag = host_seq).
 __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d, int opi) {
-  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
+  const int V = p.V, q0 = p.my_gpu * V, nd = n_deps(p, d);
   bool ok = true;
-  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
-    const int q = q0 + t / pk;
-    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+  for (int t = threadIdx.x & 31; t < V * nd; t += 32) {
+    const int q = q0 + t / nd;
+    const int src = dep_src(p, d, q, t % nd);
     if (d.stage > 0)
       ok &= wait_geq(p, ready_slot(p, q, src, opi - 1), cur_epoch(), (uint32_t)opi);
     else
@@ -550,11 +622,11 @@ __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d
 // (or the host copies of chunk c) completed?  One acquire load per flag.
 __device__ __forceinline__ bool deps_ready_warp(const KParams& p, const OpDesc& d, int opi) {
   if (d.stage == 0 && !p.host_seq) return true;
-  const int V = p.V, q0 = p.my_gpu * V, k = d.dim, pk = p.size[k];
+  const int V = p.V, q0 = p.my_gpu * V, nd = n_deps(p, d);
   bool ok = true;
-  for (int t = threadIdx.x & 31; t < V * pk; t += 32) {
-    const int q = q0 + t / pk;
-    const int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
+  for (int t = threadIdx.x & 31; t < V * nd; t += 32) {
+    const int q = q0 + t / nd;
+    const int src = dep_src(p, d, q, t % nd);
     ok &= d.stage > 0 ? dev::ld_acquire_sys(ready_slot(p, q, src, opi - 1)) >= cur_epoch()
                       : dev::ld_acquire_sys(h2d_slot(p, src / V, d.chunk)) >= p.host_seq;
   }
@@ -633,20 +705,32 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
   if (!last) return;
   if (d.next_dim >= 0) {  // (the last stage has no consumer: the exit barrier orders it)
     const int V = p.V, q0 = p.my_gpu * V, kn = d.next_dim, pn = p.size[kn];
-    // The consumers of the flag read the data next.  If all of them are on
-    // this GPU a gpu-scope release suffices; otherwise fence at sys scope.
+    // consumers of (c, s): self and the next stage's dim peers -- for a push
+    // op (R30) the whole k x k_next plane (the next stage's peers read data
+    // this op wrote into their dim-k peers)
+    const bool push = is_push(p, d);
+    const int pk = push ? p.size[d.dim] : 1;
+    const int nst = V * pn * pk;
+    auto dst_of = [&](int t, int& q) {
+      q = q0 + t / (pn * pk);
+      const int u = t % (pn * pk);
+      int dst = q + (u % pn - coord(p, q, kn)) * (int)p.stride[kn];
+      if (push) dst += (u / pn - coord(p, q, d.dim)) * (int)p.stride[d.dim];
+      return dst;
+    };
+    // If every consumer (and, for a push, every rank it wrote to) is on this
+    // GPU a gpu-scope release suffices; otherwise fence at sys scope.
     bool local = true;
-    for (int t = lane; t < V * pn; t += 32) {
-      const int q = q0 + t / pn;
-      local &= (q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn]) / V == p.my_gpu;
+    for (int t = lane; t < nst; t += 32) {
+      int q;
+      local &= dst_of(t, q) / V == p.my_gpu;
     }
     local = __all_sync(0xFFFFFFFFu, local);
     // release pattern (fence, then relaxed flag stores in the same thread's
     // program order); few flags: lane 0 alone, after one fence
-    const int nst = V * pn;
     auto publish = [&](int t) {
-      const int q = q0 + t / pn;
-      const int dst = q + (t % pn - coord(p, q, kn)) * (int)p.stride[kn];
+      int q;
+      const int dst = dst_of(t, q);
       if (local)
         dev::st_relaxed_gpu(ready_slot(p, dst, q, opi), cur_epoch());
       else
@@ -785,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
             const OpDesc& d = p.ops[opi];
             int li, wn;
             if (!op_member(d, gi, gn, li, wn)) continue;
-            if (!unit_has_work(p, d, unit_mode_tma(d), li, wn) || deps_ready_warp(p, d, opi)) pick = j;
+            if (!unit_has_work(p, d, unit_mode_tma(p, d), li, wn) || deps_ready_warp(p, d, opi)) pick = j;
           }
           if (pick < 0) {  // nothing ready yet: watchdog (decided on lane 0, warp-uniform), then scan again
             int give_up = 0;
@@ -809,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         taken |= 1u << pick;
         const int opi = list[head + pick];
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode_tma(d);
+        const int mode = unit_mode_tma(p, d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         op_member(d, gi, gn, li, wn);
@@ -866,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         if (!dev::mbar_wait_or(&q_full[slot], (n / kOpRing) & 1, p.abort_flag)) break;
         const int e = s_q[slot], opi = e >> 6, u = e & 63;
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode_tma(d);
+        const int mode = unit_mode_tma(p, d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         op_member(d, gi, gn, li, wn);
@@ -892,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         if (!__shfl_sync(0xFFFFFFFFu, w, 0)) break;
         const int e = s_q[slot], opi = e >> 6, u = e & 63;
         const OpDesc& d = p.ops[opi];
-        const int mode = unit_mode_tma(d);
+        const int mode = unit_mode_tma(p, d);
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         op_member(d, gi, gn, li, wn);

@@ -339,6 +339,11 @@ class Comm:
         """Op windows: consecutive windows (True) or every narrow op from CTA 0."""
         check(lib().themis_comm_set_window_rotation(self.h, int(rotate)))
 
+    def set_push(self, on: bool) -> None:
+        """Direct AG ops by writes (TMA bulk stores into the peers, R30);
+        takes effect at the next Plan.bind."""
+        check(lib().themis_comm_set_push(self.h, int(on)))
+
     def set_lookahead(self, lookahead: int) -> None:
         """Runtime intra-dim order: 1 = the enforced pre-simulated order;
         L > 1 = first ready op among the next L of it (direct dims, R28)."""

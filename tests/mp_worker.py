@@ -21,7 +21,7 @@ COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
 KIND_O = {th.RING: T.RING, th.DIRECT: T.DIRECT, th.SWITCH: T.SWITCH}
 
 
-def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None, lookahead=1):
+def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None, lookahead=1, push=False):
     topo = th.Topology(sizes, bw, kinds)
     P = topo.P
     V = P // W
@@ -31,6 +31,7 @@ def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, ki
     comm.set_engine(engine)
     comm.set_timeout(20.0)
     comm.set_lookahead(lookahead)
+    comm.set_push(push)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy).bind(comm)
     xs = host_inputs(P, N, dtype, dist="wide")
     for v in range(V):
@@ -131,8 +132,10 @@ def nccl_and_stress_case(group, W, g, iters=60):
         intra = rng.choice([th.SCF, th.FIFO])
         eng = rng.choice(["tma", "tma", "ldg"])
         ctas = rng.choice([None, [4, 4, 4], [12, 6, 3]])
-        key = (C, pol, intra, str(ctas))
+        push = rng.random() < 0.5                        # R30, same on every rank (launch hash)
+        key = (C, pol, intra, str(ctas), push)
         if key not in plans:
+            comm.set_push(push)
             plans[key] = th.Plan(topo, th.ALLREDUCE, N * 4, C, pol, intra).bind(comm, ctas)
         comm.set_engine(eng)
         # R28: ranks may run a dim's ops in different orders -- give every GPU
@@ -330,7 +333,7 @@ def main():
         cases.append((sizes, tuple(rng.choice([1, 2, 4]) for _ in range(D)), dtype, rng.choice([1, 4, 8]),
                       vec * rng.randint(1, 300), rng.choice([S.AR, S.AR, "RS", "AG"]),
                       rng.choice([th.THEMIS, th.BASELINE]), "tma", kinds,
-                      rng.choice([1, 4, 16])))
+                      rng.choice([1, 4, 16]), rng.random() < 0.5))
     fails = []
     for c in cases:
         if int(np.prod(c[0])) % W:

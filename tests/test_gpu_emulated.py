@@ -42,7 +42,7 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
              intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1, rotate=1,
-             lookahead=1):
+             lookahead=1, push=False):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
@@ -53,6 +53,7 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_min_cta_bytes(min_cta_bytes)
     comm.set_window_rotation(bool(rotate))
     comm.set_lookahead(lookahead)
+    comm.set_push(push)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra, concurrency=concurrency).bind(comm, ctas)
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
@@ -531,6 +532,28 @@ def test_runtime_intra_dim_order(sizes, kinds, la):
     assert P >= 8
 
 
+@pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), None), ((4, 2), None), ((2, 4), None), ((8,), None),
+                                         ((2, 3, 2), (th.DIRECT, th.RING, th.DIRECT)), ((2, 2, 2, 2), None)])
+@pytest.mark.parametrize("la", [1, 16])
+def test_push_all_gather(sizes, kinds, la):
+    """R30: direct AG ops executed as pushes (TMA bulk stores into the dim
+    peers; the next stage waits for the k x k' plane) -- AR and AG-only
+    bit-exact against the oracle, with ring dims mixed in (they stay pulls),
+    repeated calls, op windows and the runtime order."""
+    P = int(np.prod(sizes))
+    kw = dict(kinds=kinds, lookahead=la, push=True, repeat=2)
+    check_ar(sizes, (1,) * len(sizes), "i32", 16, 4 * 300, **kw)
+    check_ar(sizes, (4,) + (1,) * (len(sizes) - 1), "f32", 8, 4 * 301, dist="wide", **kw)
+    check_ar(sizes, (1,) * len(sizes), "bf16", 8, 8 * 257, dist="wide", min_cta_bytes=4096, ctas=[5] * len(sizes), **kw)
+    xs, outs = run_case(sizes, (2,) * len(sizes), "i32", 8, 4 * 129, "AG", th.THEMIS, kinds=kinds, lookahead=la,
+                        push=True)
+    N = xs[0].shape[0]
+    sched = oracle_sched(sizes, (2,) * len(sizes), "AG", N * 4, 8, th.THEMIS, kinds=kinds)
+    want = O.run_schedule(xs, sched, "i32")
+    for r in range(P):
+        assert np.array_equal(outs[r], want[r]), f"AG rank {r}"
+
+
 def test_max_ranks_and_many_chunks():
     """Edge sizes on the executor: 64 logical ranks (2^6, the per-comm
     maximum) in one GPU, and 1024 chunks (THEMIS_MAX_CHUNKS) on 2x2x2 —
@@ -602,14 +625,15 @@ def test_random_executor_configs():
         slice_elems = vec * rng.randint(1, 700)
         ctas = [rng.randint(max(2, conc), 24) for _ in range(D)]
         la = rng.choice([1, 1, 4, 16])
+        push = rng.random() < 0.4
         kw = dict(kinds=kinds, ctas=ctas, intra=intra, concurrency=conc, min_cta_bytes=0 if conc > 1 else mcb,
-                  dist="wide" if dtype != "i32" else "recipe", lookahead=la)
+                  dist="wide" if dtype != "i32" else "recipe", lookahead=la, push=push)
         try:
             check_ar(tuple(sizes), bw, dtype, C_, slice_elems, policy, **kw)
         except AssertionError as e:
             raise AssertionError(f"case {i}: sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy} "
                                  f"intra {intra} conc {conc} mcb {mcb} slice {slice_elems} ctas {ctas} "
-                                 f"lookahead {la}: {e}")
+                                 f"lookahead {la} push {push}: {e}")
 
 
 def test_random_rs_ag_configs():
