@@ -695,8 +695,9 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
   uint32_t last = 0;
   if (lane == 0) {
     if (p.tdetail) p.tdetail[6 * opi + 2] = dev::globaltimer();  // (any CTA; last writer wins)
-    last = dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
-    if (last) {
+    // a one-CTA window (small op) is complete here: no counter round trip
+    last = gn == 1 || dev::atom_add_acq_rel_gpu(&p.opcnt[opi], 1u) == (uint32_t)gn - 1;
+    if (last && gn > 1) {
       if (p.tdetail) p.tdetail[6 * opi + 3] = dev::globaltimer();
       p.opcnt[opi] = 0;  // every CTA arrived; reset for the next call
     }
