@@ -208,7 +208,13 @@ def run_themis(a):
     topo = th.Topology(SIZES, ratio, kinds)
     comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
     comm.set_timeout(30.0)
+    # runtime order pays where all dims share NVLink (head-of-line blocking of
+    # the static order: 2x2 on 4 GPUs 487 -> 638 GB/s); elsewhere it is neutral
+    # or -3 % (N = 2), profiles/r02/ (R28)
+    if not a.lookahead:
+        a.lookahead = 16 if V == 1 else 1
     comm.set_lookahead(a.lookahead)
+    comm.set_min_cta_bytes(a.min_cta_kb * 1024)
     comm.set_stages(1)
     comm.set_stage_bytes(stage_kb * 1024)
     comm.set_stages(stages)
@@ -573,6 +579,7 @@ def run_themis(a):
                                      "sharing one HBM / NVLink fabric the caps do not bind; paced rows in "
                                      "themis_vs_baseline emulate BW_K exactly)"),
                        "ops_in_flight_per_dim": max(1, a.concurrency), "intra_dim_lookahead": a.lookahead,
+                       "op_window_min_cta_kib": a.min_cta_kb,
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
                        "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages, "tma_stage_kib": stage_kb,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
@@ -699,8 +706,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stages", type=int, default=0, help="TMA ring depth (default 4 with NVLink dims, else 6)")
     ap.add_argument("--stage-kb", type=int, default=0, help="TMA ring stage size (KiB; default by topology)")
-    ap.add_argument("--lookahead", type=int, default=16,
-                    help="runtime intra-dim order: 1 = enforced pre-simulated order, L > 1 = first ready of the next L (R28)")
+    ap.add_argument("--lookahead", type=int, default=0,
+                    help="runtime intra-dim order: 1 = enforced pre-simulated order, L > 1 = first ready of the next L "
+                         "(R28); 0 = auto: 16 when every dim crosses NVLink (one rank per GPU), else 1")
+    ap.add_argument("--min-cta-kb", type=int, default=64,
+                    help="op windows: an op gets one CTA per this many KiB it moves (small ops run several per dim "
+                         "at once; 0 = every op on all its dim's CTAs)")
     ap.add_argument("--concurrency", type=int, default=1,
                     help="ops in flight per dimension in the plan's pre-simulation (1 = the paper's model)")
     ap.add_argument("--sizes", default="2,2,2", help="logical topology P_1,...,P_D (sweeps, config 3)")

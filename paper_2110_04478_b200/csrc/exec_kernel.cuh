@@ -618,31 +618,19 @@ __device__ __forceinline__ bool wait_deps_warp(const KParams& p, const OpDesc& d
   return __all_sync(0xFFFFFFFFu, ok);
 }
 
-// One lane, non-blocking: have the local ranks' and their sources' (c, s-1)
-// (or the host copies of chunk c) completed?  Flags loaded in batches of 8
-// independent acquire loads.
-__device__ __forceinline__ bool deps_ready_lane(const KParams& p, const OpDesc& d, int opi) {
+// One warp, non-blocking: have the local ranks' and their dim-k peers' (c, s-1)
+// (or the host copies of chunk c) completed?  One acquire load per flag.
+__device__ __forceinline__ bool deps_ready_warp(const KParams& p, const OpDesc& d, int opi) {
   if (d.stage == 0 && !p.host_seq) return true;
-  const int V = p.V, q0 = p.my_gpu * V, nd = n_deps(p, d), n = V * nd;
-  const uint32_t want = d.stage > 0 ? cur_epoch() : p.host_seq;
+  const int V = p.V, q0 = p.my_gpu * V, nd = n_deps(p, d);
   bool ok = true;
-  for (int b = 0; b < n && ok; b += 8) {
-    uint32_t v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = b + i;
-      if (t < n) {
-        const int q = q0 + t / nd;
-        const int src = dep_src(p, d, q, t % nd);
-        v[i] = dev::ld_acquire_sys(d.stage > 0 ? ready_slot(p, q, src, opi - 1) : h2d_slot(p, src / V, d.chunk));
-      } else {
-        v[i] = want;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ok &= v[i] >= want;
+  for (int t = threadIdx.x & 31; t < V * nd; t += 32) {
+    const int q = q0 + t / nd;
+    const int src = dep_src(p, d, q, t % nd);
+    ok &= d.stage > 0 ? dev::ld_acquire_sys(ready_slot(p, q, src, opi - 1)) >= cur_epoch()
+                      : dev::ld_acquire_sys(h2d_slot(p, src / V, d.chunk)) >= p.host_seq;
   }
-  return ok;
+  return __all_sync(0xFFFFFFFFu, ok);
 }
 
 constexpr int kFewFlags = 16;  // flag stores a single lane issues after its one release fence
@@ -875,18 +863,15 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         if (head >= nops) break;
         int pick = 0;
         if (dyn) {
-          // all candidates at once: lane j checks list[head + j]'s flags, so a
-          // scan costs one flag round trip whatever L is
-          bool rdy = false;
-          if (lane < LA && head + lane < nops && !(taken >> lane & 1u)) {
-            const int opi = list[head + lane];
+          pick = -1;
+          for (int j = 0; j < LA && head + j < nops && pick < 0; ++j) {
+            if (taken >> j & 1u) continue;
+            const int opi = list[head + j];
             const OpDesc& d = p.ops[opi];
             int li, wn;
-            if (op_member(d, gi, gn, li, wn))
-              rdy = !unit_has_work(p, d, unit_mode_tma(p, d), li, wn) || deps_ready_lane(p, d, opi);
+            if (!op_member(d, gi, gn, li, wn)) continue;
+            if (!unit_has_work(p, d, unit_mode_tma(p, d), li, wn) || deps_ready_warp(p, d, opi)) pick = j;
           }
-          const uint32_t ready = __ballot_sync(0xFFFFFFFFu, rdy);
-          pick = ready ? __ffs(ready) - 1 : -1;
           if (pick < 0) {  // nothing ready yet: watchdog (decided on lane 0, warp-uniform), then scan again
             int give_up = 0;
             if (lane == 0) {

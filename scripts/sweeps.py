@@ -36,7 +36,8 @@ from synth import WORKLOAD_PARAMS, bucket_sizes, device_input, torch_dtype  # no
 import bench  # noqa: E402
 
 CONC = 1
-LA = 1        # --lookahead: runtime intra-dim order (R28)
+LA = 0        # --lookahead: runtime intra-dim order (R28); 0 = auto (16 at one rank per GPU, else 1)
+MCB = 65536   # --min-cta-kb: op windows
 LAT = 0       # --latency-ns: measured per-op A_K for the latency-aware auto-chunk column (config 3)
 
 
@@ -50,8 +51,9 @@ class Runner:
         topo = th.Topology(tuple(sizes), (1,) * len(sizes))
         c = th.Comm(topo, max_bytes, group=self.group, device=self.local)
         c.set_timeout(30.0)
-        c.set_lookahead(LA)
         lay = bench.logical_layout(sizes, self.world)
+        c.set_lookahead(LA or (16 if lay["V"] == 1 else 1))       # R28, as bench.py's auto
+        c.set_min_cta_bytes(MCB)                                   # op windows (small ops several per dim)
         ncross = len(lay["cross_gpu_dims"])
         c.set_stages(6 if ncross < len(sizes) else (2 if len(sizes) > 1 else 4))
         self.ctas_total = self.sms if ncross == 0 else ((min(self.sms, 128) if len(sizes) > 1 else 32) if ncross == len(sizes) else
@@ -254,16 +256,18 @@ def main():
     ap.add_argument("--config", type=int, required=True, choices=[3, 4, 5])
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--concurrency", type=int, default=1, help="ops in flight per dim (plans)")
-    ap.add_argument("--lookahead", type=int, default=1, help="runtime intra-dim order window (R28)")
+    ap.add_argument("--lookahead", type=int, default=0, help="runtime intra-dim order window (R28); 0 = auto")
+    ap.add_argument("--min-cta-kb", type=int, default=64, help="op windows: KiB per CTA (0 = full-width ops)")
     ap.add_argument("--latency-ns", type=int, default=0,
                     help="config 3: also time a latency-aware Themis plan with planner-chosen chunks (A_K ns)")
     a = ap.parse_args()
     os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank, world, local, group = init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", 1)) > 1 else "gloo")
     torch.cuda.set_device(local)
-    global CONC, LAT, LA
+    global CONC, LAT, LA, MCB
     CONC = a.concurrency
     LA = a.lookahead
+    MCB = a.min_cta_kb * 1024
     LAT = a.latency_ns
     r = Runner(group, rank, world, local)
     {3: config3, 4: config4, 5: config5}[a.config](r, a.quick)
