@@ -215,3 +215,18 @@ def test_nvls_data_path_is_the_all_reduce():
     out = O.run_schedule(xs, s, "i32")
     want = O.allreduce_definition(xs, "i32")
     assert all((o == want).all() for o in out)
+
+
+def test_nvls_fixed_delay_seed_and_charge():
+    """R29 A_K of the fused pair = 2 steps (reduce + multicast) x step_latency.
+    D = 1, P = 4, NVLS, step latency 700 ns, S = 64 B, C = 4, BW 1 B/ns:
+      tracker seed (AR) = 2 x 700 = 1400 (a plain switch dim: 2 phases x
+      log2 4 steps x 700 = 2800); final tracker = 1400 + 4 x 20 = 1480;
+      with per-op latency charged each fused op takes 20 + 1400 ns and its AG
+      half 0 -> makespan 4 x 1420 = 5680."""
+    t = T.Topology.make((4,), (1,), (T.NVLS,), (700,))
+    s = S.schedule_collective(t, S.AR, 64, 4, S.THEMIS)
+    assert S.tracker_reset(t, S.AR) == [1400]
+    assert S.tracker_reset(T.Topology.make((4,), (1,), (T.SWITCH,), (700,)), S.AR) == [2800]
+    assert s.loads == [1480]
+    assert E.simulate(s, E.SCF, charge_latency=True).makespan == 5680
