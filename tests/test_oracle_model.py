@@ -45,6 +45,10 @@ def test_topology_validation_and_coords():
     with pytest.raises(ValueError):
         T.Topology.make((6,), (1,), (T.SWITCH,))          # SPEC.md:39 power-of-two rule
     with pytest.raises(ValueError):
+        T.Topology.make((6,), (1,), (T.NVLS,))            # R29: a switch that reduces, same rule
+    with pytest.raises(ValueError):
+        T.Topology.make((4,), (0,))                        # BW > 0
+    with pytest.raises(ValueError):
         T.Topology.make((1, 4), (1, 1))
     t = T.Topology.make((2, 4, 3), (1, 1, 1))
     for r in range(t.P):
@@ -52,6 +56,11 @@ def test_topology_validation_and_coords():
     assert t.coords(1) == (1, 0, 0)                         # dim1 fastest
     assert t.coords(2) == (0, 1, 0)
     assert t.dim_peers(0, 1) == [0, 2, 4, 6]
+    # dim peers by brute force: ranks whose coordinates differ from r only on dim k
+    for r in range(t.P):
+        for k in range(t.D):
+            want = [q for q in range(t.P) if all(t.coords(q)[i] == t.coords(r)[i] for i in range(t.D) if i != k)]
+            assert sorted(t.dim_peers(r, k)) == want
 
 
 # ---------------------------------------------------------------- collectives
