@@ -208,11 +208,12 @@ def run_themis(a):
     topo = th.Topology(SIZES, ratio, kinds)
     comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
     comm.set_timeout(30.0)
-    # runtime order pays where all dims share NVLink (head-of-line blocking of
-    # the static order: 2x2 on 4 GPUs 487 -> 638 GB/s); elsewhere it is neutral
-    # or -3 % (N = 2), profiles/r02/ (R28)
+    # runtime order pays where NVLink dims dominate (head-of-line blocking of
+    # the static order: 2x2 on 4 GPUs 487 -> 638 GB/s; 2x2x2 at N = 4 caps
+    # 1:1:1 baseline 421 -> 622); neutral at N = 1, -3 % on the N = 2 headline
+    # (profiles/r02/, R28)
     if not a.lookahead:
-        a.lookahead = 16 if V == 1 else 1
+        a.lookahead = 16 if V <= 2 else 1
     comm.set_lookahead(a.lookahead)
     comm.set_min_cta_bytes(a.min_cta_kb * 1024)
     comm.set_stages(1)
@@ -708,7 +709,7 @@ def main():
     ap.add_argument("--stage-kb", type=int, default=0, help="TMA ring stage size (KiB; default by topology)")
     ap.add_argument("--lookahead", type=int, default=0,
                     help="runtime intra-dim order: 1 = enforced pre-simulated order, L > 1 = first ready of the next L "
-                         "(R28); 0 = auto: 16 when every dim crosses NVLink (one rank per GPU), else 1")
+                         "(R28); 0 = auto: 16 with <= 2 ranks per GPU, else 1")
     ap.add_argument("--min-cta-kb", type=int, default=64,
                     help="op windows: an op gets one CTA per this many KiB it moves (small ops run several per dim "
                          "at once; 0 = every op on all its dim's CTAs)")

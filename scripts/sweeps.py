@@ -36,7 +36,7 @@ from synth import WORKLOAD_PARAMS, bucket_sizes, device_input, torch_dtype  # no
 import bench  # noqa: E402
 
 CONC = 1
-LA = 0        # --lookahead: runtime intra-dim order (R28); 0 = auto (16 at one rank per GPU, else 1)
+LA = 0        # --lookahead: runtime intra-dim order (R28); 0 = auto (16 at <= 2 ranks per GPU, else 1)
 MCB = 65536   # --min-cta-kb: op windows
 LAT = 0       # --latency-ns: measured per-op A_K for the latency-aware auto-chunk column (config 3)
 
@@ -52,7 +52,7 @@ class Runner:
         c = th.Comm(topo, max_bytes, group=self.group, device=self.local)
         c.set_timeout(30.0)
         lay = bench.logical_layout(sizes, self.world)
-        c.set_lookahead(LA or (16 if lay["V"] == 1 else 1))       # R28, as bench.py's auto
+        c.set_lookahead(LA or (16 if lay["V"] <= 2 else 1))       # R28, as bench.py's auto
         c.set_min_cta_bytes(MCB)                                   # op windows (small ops several per dim)
         ncross = len(lay["cross_gpu_dims"])
         c.set_stages(6 if ncross < len(sizes) else (2 if len(sizes) > 1 else 4))
