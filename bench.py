@@ -48,6 +48,37 @@ def logical_layout(sizes, n_gpus):
     return {"P": P, "V": V, "cross_gpu_dims": cross}
 
 
+def launch_config(sizes, n_gpus, sms, nvls=False):
+    """bench.py's launch configuration for a logical topology on n_gpus GPUs
+    (also used by the full-size parity tests, so they check exactly what is
+    timed):
+      CTA budget / TMA ring (K5 calibration, profiles/r01_nvlink_calibration.md,
+      profiles/r02/ceilings): NVLink saturates with a bounded amount in flight
+      per GPU (all-NVLink best at 128 CTAs x 2 x 32 KiB; more stages lose);
+      HBM-resident dims want every SM and larger tiles (3 x 64 KiB at N = 1,
+      4 x 48 KiB mixed);
+      runtime intra-dim order (R28): L = 16 with <= 2 ranks per GPU (head-of-line
+      blocking of the static order where NVLink dims dominate: 2x2 on 4 GPUs
+      487 -> 638 GB/s), else the enforced order (neutral at N = 1, -3 % on the
+      N = 2 headline)."""
+    lay = logical_layout(sizes, n_gpus)
+    V, ncross = lay["V"], len(lay["cross_gpu_dims"])
+    if ncross == 0:
+        total = sms
+    elif ncross == len(sizes):
+        total = min(sms, 128) if len(sizes) > 1 else (64 if nvls else 32)   # NVLS wants more threads in flight
+    else:
+        total = sms if V >= 4 else 96
+    if ncross == len(sizes):
+        stages, kb = (2 if len(sizes) > 1 else 4), 32
+    elif ncross == 0:
+        stages, kb = 3, 64
+    else:
+        stages, kb = 4, 48
+    return {"total_ctas": total, "stages": stages, "stage_kb": kb, "lookahead": 16 if V <= 2 else 1,
+            "min_cta_bytes": 64 * 1024}
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -181,39 +212,14 @@ def run_themis(a):
     N = S // 4
     ratio = tuple(int(x) for x in a.ratio.split(":"))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # CTA budget / TMA ring depth (K5 calibration, profiles/r01_nvlink_calibration.md):
-    # NVLink saturates with ~4 MB in flight per GPU (32 CTAs x 4 x 32 KiB);
-    # more in-flight requests lose bandwidth.  HBM-resident dims want all SMs.
-    ncross_ = len(lay["cross_gpu_dims"])
-    if a.ctas_total:
-        total_ctas = a.ctas_total
-    elif ncross_ == 0:
-        total_ctas = sms
-    elif ncross_ == len(SIZES):   # every dim over NVLink (calibration: 2x2 best at 128 CTAs x 2 x 32 KiB)
-        total_ctas = min(sms, 128) if len(SIZES) > 1 else (64 if a.nvls else 32)   # NVLS wants more threads in flight
-    else:   # mixed: GPU-local dims (HBM) want many CTAs
-        total_ctas = sms if V >= 4 else 96
-    # TMA ring (stages x stage bytes, <= 192 KiB): larger tiles cut the fixed
-    # per-tile cost (profiles/r01/stagekb/: 3 x 64 KiB +0.8 % at N = 1, 4 x 48
-    # KiB +2 % at N = 4 over 6 x 32); all-NVLink topologies peak with ~8 MB in
-    # flight per GPU, spread over many CTAs (scripts/grid.py --preset hier-ring: 128 CTAs
-    # x 2 x 32 KiB 627 vs 96 x 3 x 32 KiB 600 GB/s on 2x2)
-    if ncross_ == len(SIZES):
-        stages, stage_kb = a.stages or (2 if len(SIZES) > 1 else 4), a.stage_kb or 32
-    elif ncross_ == 0:
-        stages, stage_kb = a.stages or 3, a.stage_kb or 64
-    else:
-        stages, stage_kb = a.stages or 4, a.stage_kb or 48
+    cfg = launch_config(SIZES, world, sms, nvls=a.nvls)
+    total_ctas = a.ctas_total or cfg["total_ctas"]
+    stages, stage_kb = a.stages or cfg["stages"], a.stage_kb or cfg["stage_kb"]
     kinds = (th.NVLS,) * len(SIZES) if a.nvls else None   # NVSwitch dims with in-switch reduction where eligible (R27, R29)
     topo = th.Topology(SIZES, ratio, kinds)
     comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
     comm.set_timeout(30.0)
-    # runtime order pays where NVLink dims dominate (head-of-line blocking of
-    # the static order: 2x2 on 4 GPUs 487 -> 638 GB/s; 2x2x2 at N = 4 caps
-    # 1:1:1 baseline 421 -> 622); neutral at N = 1, -3 % on the N = 2 headline
-    # (profiles/r02/, R28)
-    if not a.lookahead:
-        a.lookahead = 16 if V <= 2 else 1
+    a.lookahead = a.lookahead or cfg["lookahead"]
     comm.set_lookahead(a.lookahead)
     comm.set_min_cta_bytes(a.min_cta_kb * 1024)
     comm.set_stages(1)

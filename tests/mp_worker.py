@@ -72,15 +72,17 @@ def fullsize_case(group, W, g):
     S_ = 1 << 30
     N = S_ // 4
     topo = th.Topology(sizes, ratio)
-    lay = bench.logical_layout(sizes, W)
-    V = lay["V"]
-    ncross = len(lay["cross_gpu_dims"])
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    total = sms if ncross == 0 else (32 * 3 + 32 if ncross == 3 else (sms if V >= 4 else 96))
+    cfg = bench.launch_config(sizes, W, sms)               # exactly what bench.py times
+    V = bench.logical_layout(sizes, W)["V"]
     comm = th.Comm(topo, S_, group=group)
     comm.set_timeout(30.0)
-    comm.set_stages(3 if ncross == 3 else 4)
-    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, th.default_ctas(ratio, total))
+    comm.set_stages(1)
+    comm.set_stage_bytes(cfg["stage_kb"] * 1024)
+    comm.set_stages(cfg["stages"])
+    comm.set_lookahead(cfg["lookahead"])
+    comm.set_min_cta_bytes(cfg["min_cta_bytes"])
+    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, th.default_ctas(ratio, cfg["total_ctas"]))
     from synth import device_input
     xs = [device_input(g * V + v, N, "f32", torch.device("cuda")) for v in range(V)]
     for v in range(V):

@@ -44,3 +44,18 @@ def test_paced_bw_exact_ratio():
         bw = bench.paced_bw(rat, 500.0)
         assert all(Fraction(b, bw[0]) == Fraction(r, rat[0]) for b, r in zip(bw, rat))
         assert sum(bw) <= 500_000 + 1000 * len(rat) and all(b % 1000 == 0 for b in bw)
+
+
+def test_launch_config_per_gpu_count():
+    """bench.py's launch configuration (shared with the full-size parity
+    tests): every-SM HBM runs at N = 1, the mixed and all-NVLink budgets, the
+    runtime order where <= 2 ranks share a GPU."""
+    c1 = bench.launch_config((2, 2, 2), 1, 148)
+    assert (c1["total_ctas"], c1["stages"], c1["stage_kb"], c1["lookahead"]) == (148, 3, 64, 1)
+    c2 = bench.launch_config((2, 2, 2), 2, 148)
+    assert (c2["total_ctas"], c2["stages"], c2["stage_kb"], c2["lookahead"]) == (148, 4, 48, 1)
+    c4 = bench.launch_config((2, 2, 2), 4, 148)
+    assert (c4["total_ctas"], c4["stages"], c4["stage_kb"], c4["lookahead"]) == (96, 4, 48, 16)
+    c8 = bench.launch_config((2, 2, 2), 8, 148)
+    assert (c8["total_ctas"], c8["stages"], c8["stage_kb"], c8["lookahead"]) == (128, 2, 32, 16)
+    assert all(c["stages"] * c["stage_kb"] <= 192 for c in (c1, c2, c4, c8))

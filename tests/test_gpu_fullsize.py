@@ -35,10 +35,16 @@ def test_config2_full_size(dtype):
     P = topo.P
     S_ = MIB << 20
     N = S_ // 4
-    comm = th.Comm(topo, S_)
-    comm.set_stages(6)
+    import bench
+    cfg = bench.launch_config(SIZES, 1, torch.cuda.get_device_properties(0).multi_processor_count)
+    comm = th.Comm(topo, S_)                            # bench.py's N = 1 launch configuration
+    comm.set_stages(1)
+    comm.set_stage_bytes(cfg["stage_kb"] * 1024)
+    comm.set_stages(cfg["stages"])
+    comm.set_lookahead(cfg["lookahead"])
+    comm.set_min_cta_bytes(cfg["min_cta_bytes"])
     comm.set_timeout(30.0)
-    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, [85, 42, 21])
+    plan = th.Plan(topo, th.ALLREDUCE, S_, C, th.THEMIS).bind(comm, th.default_ctas(RATIO, cfg["total_ctas"]))
     try:
         xs = [device_input(r, N, dtype, torch.device("cuda", 0)) for r in range(P)]
         for r in range(P):
