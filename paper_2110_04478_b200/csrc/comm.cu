@@ -86,7 +86,6 @@ struct themis_comm {
   double min_cta_bytes = 0.0;  // op window sizing, 0 = full-width ops (themis_comm_set_min_cta_bytes)
   int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
   int lookahead = 1;           // runtime intra-dim order window (themis_comm_set_lookahead); 1 = static
-  uint32_t exp = 0;            // experiment bits (env THEMIS_EXP)
   int push_ag = 0;             // direct AG ops as pushes (themis_comm_set_push, R30); applies at bind
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
@@ -218,7 +217,6 @@ extern "C" themis_status_t themis_comm_create(int32_t gpu_rank, int32_t n_gpus, 
   if (const char* env = getenv("THEMIS_MIN_CTA_BYTES")) c->min_cta_bytes = std::max(0.0, atof(env));
   if (const char* env = getenv("THEMIS_WINDOW_ROTATE")) c->window_rotate = atoi(env) != 0;
   if (const char* env = getenv("THEMIS_PUSH")) c->push_ag = atoi(env) != 0;
-  if (const char* env = getenv("THEMIS_EXP")) c->exp = (uint32_t)strtoul(env, nullptr, 0);
   if (const char* env = getenv("THEMIS_LOOKAHEAD")) c->lookahead = std::max(1, std::min(kMaxLookahead, atoi(env)));
   c->max_blocks = nb * c->num_sms;
   *out = c;
@@ -650,7 +648,6 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.plan_hash = launch_hash(pl, count, dtype);
   kp.lookahead = c->lookahead;
   kp.push_ok = c->engine && !host_seq;  // host streaming publishes per-chunk d2h flags from the last stage: pull
-  kp.exp = c->exp;
   kp.dyn_mask = pl->bind->dyn_mask;
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;

@@ -69,7 +69,6 @@ struct KParams {
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes, leaky bucket (0 = off)
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
   uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
-  uint32_t exp;             // experiment bits (env THEMIS_EXP; 0 = the documented protocol)
   int32_t push_ok;          // push AG allowed in this launch (off while host-buffer streaming)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
