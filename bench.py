@@ -79,6 +79,17 @@ def launch_config(sizes, n_gpus, sms, nvls=False):
             "min_cta_bytes": 64 * 1024}
 
 
+def calibrated_bw(rates_gbs, group=None, device=None):
+    """Per-dim BW (MB/s) for a calibrated Themis plan from this rank's measured
+    per-dim rates (GB/s): the minimum over ranks (every rank must build the
+    identical plan, R22), quantised to 1/32 of the fastest dim's rate (keeps
+    lcm(BW) -- the planner's exact time scale -- small, R21)."""
+    from paper_2110_04478_b200.dist import max_over_ranks
+    r = [-max_over_ranks(-float(x), group, device) for x in rates_gbs]
+    q = max(1.0, max(r) / 32)
+    return tuple(max(1, int(round(x / q))) * int(round(q * 1000)) for x in r)
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -293,7 +304,7 @@ def run_themis(a):
                     ce = max(ce, e0)
             busy += ce - cs
             nk = plan.info["dim_volume"][k] / plan.info["byte_scale"]
-            out.append(-max_over_ranks(-(nk / max(busy, 1)), group, dev))
+            out.append(nk / max(busy, 1))
         return out
 
     main = make(th.THEMIS, ratio)
@@ -350,8 +361,7 @@ def run_themis(a):
                     # quantised to 1/32 of the fastest dim's rate (keeps lcm(BW) -- the
                     # planner's exact time scale -- small; R21)
                     def cal_plan(rates):
-                        q = max(1.0, max(rates) / 32)
-                        cal = tuple(max(1, int(round(r / q))) * int(round(q * 1000)) for r in rates)
+                        cal = calibrated_bw(rates, group, dev)
                         pc_ = th.Plan(th.Topology(SIZES, cal, kinds), th.ALLREDUCE, S, a.chunks, th.THEMIS, th.SCF)
                         check_same_plan(pc_, group)
                         return pc_.bind(comm, caps_for(rat))

@@ -95,3 +95,36 @@ def test_rank_layout_helpers():
     assert lay["V"] == 4 and lay["cross_gpu_dims"] == [2]
     lay = logical_layout((2, 2, 2), 1)
     assert lay["V"] == 8 and lay["cross_gpu_dims"] == []
+
+
+def _cal_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import bench
+    from paper_2110_04478_b200.dist import init_from_env
+    r, w, local, group = init_from_env("gloo")
+    try:
+        # each rank measured slightly different per-dim rates
+        rates = [412.3 + 3 * r, 207.9 - r, 101.4 + 0.5 * r]
+        q.put((r, bench.calibrated_bw(rates, group)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_calibrated_bw_identical_on_every_rank():
+    """bench's calibrated-BW plan input: min over ranks, quantised -- the same
+    tuple on every rank (else the ranks would launch different plans, R22)."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_cal_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(world))
+    assert res[0][1] == res[1][1]
+    q_ = 412.3 / 32                                          # min over ranks, quantum = fastest / 32
+    assert res[0][1] == tuple(round(x / q_) * round(q_ * 1000) for x in (412.3, 206.9, 101.4))
