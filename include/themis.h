@@ -264,8 +264,8 @@ themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rot
 themis_status_t themis_comm_set_push(themis_comm_t* comm, int32_t on);
 /* Runtime intra-dimension order (DESIGN R28).  lookahead = 1
  * (default, env THEMIS_LOOKAHEAD): every dimension group runs its ops in the
- * pre-simulated enforced order.  L in 2..32: on dims that
- * run the direct algorithm (no ring steps, no NVLS op), each CTA's producer
+ * pre-simulated enforced order.  L in 2..32: on every dim
+ * without ring steps (direct, switch and NVLS dims), each CTA's producer
  * takes, among the next L not-yet-taken ops of the enforced list, the first
  * whose dependencies already hold (the enforced order stays the priority;
  * readiness decides), so a late op no longer blocks ready ones behind it.

@@ -108,7 +108,7 @@ struct BindState {
   int32_t ctas[THEMIS_MAX_DIMS] = {};
   int32_t total_ctas = 0;
   bool nvls = false;  // some op runs through the switch (TMA engine only)
-  uint32_t dyn_mask = 0;  // dims whose ops may take the runtime order (direct algorithm, no NVLS op)
+  uint32_t dyn_mask = 0;  // dims whose ops may take the runtime order (no ring steps)
   int32_t nvls_pairs = 0;  // RS+AG pairs running in the switch
   uint64_t desc_hash = 0;  // of the uploaded op windows / algorithms (mixed into the launch's plan hash)
 };
@@ -509,7 +509,7 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   b->nvls_pairs = n_fused;
   b->dyn_mask = (1u << D) - 1;
   for (const OpDesc& d : ops)
-    if (d.ring || d.nvls) b->dyn_mask &= ~(1u << d.dim);
+    if (d.ring) b->dyn_mask &= ~(1u << d.dim);  // ring-step flags assume the same op order on neighbours
   pl->bind = b;
   c->bound.push_back(pl);
   return THEMIS_OK;

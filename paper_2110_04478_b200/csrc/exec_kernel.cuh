@@ -68,7 +68,7 @@ struct KParams {
   uint64_t* tdetail;        // [C*NS*6] detailed per-op stamps (trace level 2) or null
   float pace_ns_per_byte[THEMIS_MAX_DIMS];  // per-CTA pacing of peer bytes, leaky bucket (0 = off)
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
-  uint32_t dyn_mask;        // dims whose ops may be reordered at run time (direct algorithm, no NVLS)
+  uint32_t dyn_mask;        // dims whose ops may be reordered at run time (no ring steps)
   int32_t push_ok;          // push AG allowed in this launch (off while host-buffer streaming)
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
@@ -824,8 +824,8 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
     // tile stream.  The producer announces every unit it takes (op, ring step)
     // in a shared-memory queue that the consumers and the completion warp
     // follow, so the order is the producer's alone:
-    //   static (default; ring dims, NVLS): the enforced order;
-    //   runtime (lookahead L > 1, direct dims): the first op among the next L
+    //   static (default; ring dims): the enforced order;
+    //   runtime (lookahead L > 1, non-ring dims): the first op among the next L
     //   not-yet-taken ops of the enforced list whose dependencies already
     //   hold -- the pre-simulated order is the priority, readiness decides
     //   (SURVEY NEXT-3, R28).  Pull-based ops only read peers' finished
