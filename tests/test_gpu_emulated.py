@@ -653,13 +653,14 @@ def test_random_rs_ag_configs():
         policy = rng.choice([th.THEMIS, th.BASELINE])
         coll = rng.choice(["RS", "AG"])
         slice_elems = (16 // ELEM_SIZE[dtype]) * rng.randint(1, 500)
+        la, push, mcb = rng.choice([1, 1, 8]), rng.random() < 0.4, rng.choice([0, 0, 4096])
         xs, outs = run_case(sizes, bw, dtype, C_, slice_elems, coll, policy, kinds=kinds,
-                            dist="wide" if dtype != "i32" else "recipe")
+                            dist="wide" if dtype != "i32" else "recipe", lookahead=la, push=push, min_cta_bytes=mcb)
         P, N = len(xs), xs[0].shape[0]
         sched = oracle_sched(sizes, bw, coll, N * ELEM_SIZE[dtype], C_, policy, kinds=kinds)
         tree = O.run_schedule(xs, sched, dtype)
         blk = N // P
-        msg = f"case {i}: {coll} sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy}"
+        msg = f"case {i}: {coll} sizes {sizes} kinds {kinds} bw {bw} {dtype} C {C_} policy {policy} la {la} push {push} mcb {mcb}"
         for r in range(P):
             got = outs[r][r * blk:(r + 1) * blk] if coll == "RS" else outs[r]
             want = tree[r][r * blk:(r + 1) * blk] if coll == "RS" else tree[r]
