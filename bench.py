@@ -228,8 +228,12 @@ def run_themis(a):
     stages, stage_kb = a.stages or cfg["stages"], a.stage_kb or cfg["stage_kb"]
     kinds = (th.NVLS,) * len(SIZES) if a.nvls else None   # NVSwitch dims with in-switch reduction where eligible (R27, R29)
     topo = th.Topology(SIZES, ratio, kinds)
-    comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1)
+    ll_max = a.ll_max_mib << 20
+    comm = th.Comm(topo, S, group=group, device=local, nvls=a.nvls and world > 1,
+                   ll_bytes=4 * min(S, ll_max) if ll_max else 0)
     comm.set_timeout(30.0)
+    if ll_max:
+        comm.set_ll(ll_max)
     a.lookahead = a.lookahead or cfg["lookahead"]
     comm.set_lookahead(a.lookahead)
     comm.set_min_cta_bytes(a.min_cta_kb * 1024)
@@ -596,7 +600,7 @@ def run_themis(a):
                                      "sharing one HBM / NVLink fabric the caps do not bind; paced rows in "
                                      "themis_vs_baseline emulate BW_K exactly)"),
                        "ops_in_flight_per_dim": max(1, a.concurrency), "intra_dim_lookahead": a.lookahead,
-                       "op_window_min_cta_kib": a.min_cta_kb,
+                       "op_window_min_cta_kib": a.min_cta_kb, "ll": main.bound_ll(),
                        "cross_gpu_dims": [k + 1 for k in lay["cross_gpu_dims"]],
                        "ctas_per_dim": main.bound_ctas(), "engine": "tma", "tma_stages": stages, "tma_stage_kib": stage_kb,
                        "value_definition": "bus GB/s per logical rank = 2 S (P-1)/P / t, t = max over GPUs",
@@ -717,6 +721,8 @@ def main():
                     help="per-op A_K for the latency-aware auto-chunk compare rows (default: measured 8.5 / 11 us)")
     ap.add_argument("--cpu-mib", type=int, default=256, help="oracle sample size per rank (MiB)")
     ap.add_argument("--pace-gbs", type=float, default=0, help="per-rank sum of paced dim BWs (GB/s)")
+    ap.add_argument("--ll-max-mib", type=int, default=0,
+                    help="LL packets (R31) for collectives of at most this many MiB per rank (0 = off)")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--nccl", action="store_true", help="NCCL context row even with --no-compare")
     ap.add_argument("--no-e2e", action="store_true")

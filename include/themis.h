@@ -251,6 +251,22 @@ themis_status_t themis_comm_set_min_cta_bytes(themis_comm_t* comm, uint64_t byte
  * small op occupies (and synchronises) only the CTAs it needs.  Takes effect at
  * the next themis_plan_bind.  Errors: INVALID_ARG. */
 themis_status_t themis_comm_set_window_rotation(themis_comm_t* comm, int32_t rotate);
+/* LL small collectives (DESIGN R31).  inbox_bytes > 0: every local rank has
+ * an inbox of inbox_bytes right after the heap's data regions (the caller
+ * allocated heap_bytes >= V * (signal_bytes + vrank_stride + inbox_bytes);
+ * 16-byte multiple).  At the next themis_plan_bind, a plan of at most
+ * max_bytes with no ring dim and no NVLS pair whose ops' inbox regions fit
+ * (sum over ops of (P_k - 1) x part x 2) runs EVERY op with LL packets: the
+ * sender stores 8-byte {4 payload bytes, epoch} packets straight into the
+ * receivers' inboxes and the receivers poll the packets -- no flag, fence or
+ * read round trip between ranks (each op waits only for its own previous
+ * stage); the per-dim orders stay the enforced ones (the exchange is
+ * pairwise, like the paper's collective ops).  Same summation order as the
+ * pull path: results bit-identical.  themis_plan_bound_ll reports whether a
+ * bound plan runs LL.  Host-buffer streaming and the LDG engine refuse LL
+ * plans.  All ranks must use the same setting (launch hash).
+ * Errors: INVALID_ARG (does not fit the heap). */
+themis_status_t themis_comm_set_ll(themis_comm_t* comm, uint64_t inbox_bytes, uint64_t max_bytes);
 /* Push-mode All-Gather (DESIGN R30): on = 1 (env THEMIS_PUSH), at the next
  * themis_plan_bind every direct-algorithm AG op (not ring, not NVLS) runs by
  * WRITES: each rank streams its own held part through shared memory and TMA
@@ -334,6 +350,9 @@ themis_status_t themis_plan_launch_hash(const themis_plan_t* plan, uint64_t coun
  * profiled (ncu replays it) with real NVLink traffic.  Results are garbage.
  * Errors: PLAN_MISMATCH (not bound), INVALID_ARG, CUDA. */
 themis_status_t themis_debug_fake_peer_gpu(const themis_plan_t* plan, int32_t peer_gpu, uint64_t count, int32_t dtype);
+/* 1 if a bound plan runs with LL packets (R31), else 0.
+ * Errors: PLAN_MISMATCH if the plan is not bound. */
+themis_status_t themis_plan_bound_ll(const themis_plan_t* plan, int32_t* ll /*[host,out]*/);
 /* Number of a bound plan's chunk RS+AG pairs that run as in-switch
  * All-Reduces (NVLS dims on a multicast-capable comm, R29); 0 otherwise.
  * Errors: PLAN_MISMATCH if the plan is not bound. */

@@ -79,6 +79,8 @@ SIGNATURES = {
     "themis_comm_set_window_rotation": (_ST, [_P, C.c_int32]),
     "themis_comm_set_lookahead": (_ST, [_P, C.c_int32]),
     "themis_comm_set_push": (_ST, [_P, C.c_int32]),
+    "themis_comm_set_ll": (_ST, [_P, C.c_uint64, C.c_uint64]),
+    "themis_plan_bound_ll": (_ST, [_P, C.POINTER(C.c_int32)]),
     "themis_comm_set_multicast": (_ST, [_P, _P]),
     "themis_comm_set_timeout": (_ST, [_P, C.c_uint64]),
     "themis_comm_enable_trace": (_ST, [_P, C.c_int32]),

@@ -87,6 +87,8 @@ struct themis_comm {
   int window_rotate = 1;       // consecutive windows (1) or all from CTA 0 (0) (themis_comm_set_window_rotation)
   int lookahead = 1;           // runtime intra-dim order window (themis_comm_set_lookahead); 1 = static
   int push_ag = 0;             // direct AG ops as pushes (themis_comm_set_push, R30); applies at bind
+  uint64_t ll_stride = 0;      // LL inbox bytes per local rank after the data regions (themis_comm_set_ll, R31)
+  uint64_t ll_max_bytes = 0;   // plans of at most this many bytes run LL (0 = never)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   int max_blocks = 0;  // co-resident CTAs for the kernel
   int engine = 1;      // 1: TMA bulk-copy pipeline, 0: LDG/STG
@@ -110,6 +112,7 @@ struct BindState {
   bool nvls = false;  // some op runs through the switch (TMA engine only)
   uint32_t dyn_mask = 0;  // dims whose ops may take the runtime order (no ring steps)
   int32_t nvls_pairs = 0;  // RS+AG pairs running in the switch
+  bool ll = false;         // every op runs with LL packets (R31)
   uint64_t desc_hash = 0;  // of the uploaded op windows / algorithms (mixed into the launch's plan hash)
 };
 }  // namespace themis
@@ -267,6 +270,15 @@ extern "C" themis_status_t themis_comm_set_window_rotation(themis_comm_t* c, int
   c->window_rotate = rotate;
   return THEMIS_OK;
 }
+extern "C" themis_status_t themis_comm_set_ll(themis_comm_t* c, uint64_t inbox_bytes, uint64_t max_bytes) {
+  if (!c) return fail(THEMIS_ERR_INVALID_ARG, "null comm");
+  if (inbox_bytes % 16 ||
+      (uint64_t)c->V * (c->sig_bytes + c->vrank_stride + inbox_bytes) > c->heap_bytes)
+    return fail(THEMIS_ERR_INVALID_ARG, "LL inboxes (16-byte multiple, V per GPU after the data regions) do not fit the heap");
+  c->ll_stride = inbox_bytes;
+  c->ll_max_bytes = inbox_bytes ? max_bytes : 0;
+  return THEMIS_OK;
+}
 extern "C" themis_status_t themis_comm_set_push(themis_comm_t* c, int32_t on) {
   if (!c || on < 0 || on > 1) return fail(THEMIS_ERR_INVALID_ARG, "push must be 0 or 1");
   c->push_ag = on;
@@ -422,6 +434,28 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     ops[i].push = c->push_ag && ops[i].phase == 1 && !ops[i].ring && !ops[i].nvls;
   }
   for (size_t i = 0; i < ops.size(); ++i) ops[i].prev_push = ops[i].stage > 0 && ops[i - 1].push;
+  // R31: a small collective (bytes <= ll_max_bytes, no ring dims, no NVLS
+  // pair) runs every op with LL packets; each op gets a region of every
+  // rank's inbox: (P_k - 1) sources x the rank's part (nblk slices) x 2
+  // (8-byte packets carry 4 payload bytes)
+  bool ll = c->ll_max_bytes && pl->req.bytes <= c->ll_max_bytes && !any_nvls;
+  for (const OpDesc& d : ops) ll = ll && !d.ring;
+  if (ll) {
+    const uint64_t slice = pl->req.bytes / ((uint64_t)pl->P * pl->C);
+    uint64_t off = 0;
+    for (OpDesc& d : ops) {
+      d.ll = 1;
+      d.push = 0;
+      d.prev_push = 0;
+      d.ll_off = off;
+      off += (uint64_t)(pl->topo.size[d.dim] - 1) * (uint64_t)d.nblk * slice * 2;
+    }
+    if (off > c->ll_stride) ll = false;
+    if (!ll)
+      for (OpDesc& d : ops) d.ll = 0, d.ll_off = 0, d.push = c->push_ag && d.phase == 1 && !d.ring && !d.nvls;
+    if (!ll)
+      for (size_t i = 0; i < ops.size(); ++i) ops[i].prev_push = ops[i].stage > 0 && ops[i - 1].push;
+  }
   std::vector<int32_t> lists((size_t)D * pl->C * pl->NS, 0);
   for (int k = 0; k < D; ++k)
     for (size_t i = 0; i < pl->dim_ops[k].size(); ++i) {
@@ -482,6 +516,8 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
     mix(d.nvls);
     mix(d.seq);
     mix(d.push);
+    mix(d.ll);
+    mix((int64_t)d.ll_off);
     uint32_t ps;
     std::memcpy(&ps, &d.pace_scale, 4);
     mix(ps);
@@ -509,7 +545,8 @@ extern "C" themis_status_t themis_plan_bind(themis_plan_t* pl, themis_comm_t* c,
   b->nvls_pairs = n_fused;
   b->dyn_mask = (1u << D) - 1;
   for (const OpDesc& d : ops)
-    if (d.ring) b->dyn_mask &= ~(1u << d.dim);  // ring-step flags assume the same op order on neighbours
+    if (d.ring || d.ll) b->dyn_mask &= ~(1u << d.dim);  // ring steps / LL packets: the same op order on every rank
+  b->ll = !ops.empty() && ops[0].ll;
   pl->bind = b;
   c->bound.push_back(pl);
   return THEMIS_OK;
@@ -552,6 +589,12 @@ extern "C" themis_status_t themis_debug_fake_peer_gpu(const themis_plan_t* pl, i
       CUDA_TRY(cudaMemcpy(pad + hash_offset(P) + 8ull * src, &h, 8, cudaMemcpyHostToDevice));  // plan hash
     }
   }
+  return THEMIS_OK;
+}
+
+extern "C" themis_status_t themis_plan_bound_ll(const themis_plan_t* pl, int32_t* ll) {
+  if (!pl || !pl->bind || !ll) return fail(THEMIS_ERR_PLAN_MISMATCH, "plan not bound");
+  *ll = pl->bind->ll;
   return THEMIS_OK;
 }
 
@@ -647,7 +690,9 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
   kp.tdetail = c->trace_on >= 2 ? c->trace + 2 * kMaxOps : nullptr;
   kp.plan_hash = launch_hash(pl, count, dtype);
   kp.lookahead = c->lookahead;
-  kp.push_ok = c->engine && !host_seq;  // host streaming publishes per-chunk d2h flags from the last stage: pull
+  kp.push_ok = c->engine && !host_seq;
+  kp.ll_rel = (uint64_t)c->V * (c->sig_bytes + c->vrank_stride);
+  kp.ll_stride = c->ll_stride;  // host streaming publishes per-chunk d2h flags from the last stage: pull
   kp.dyn_mask = pl->bind->dyn_mask;
   kp.stages = c->stages;
   kp.stage_bytes = c->stage_bytes;
@@ -666,6 +711,8 @@ static themis_status_t launch(int coll, void* buf, uint64_t count, int32_t dtype
         return fail(THEMIS_ERR_INVALID_ARG, "ring dimensions need the TMA engine (themis_comm_set_engine(comm, 1))");
   if (!c->engine && pl->bind->nvls)
     return fail(THEMIS_ERR_INVALID_ARG, "NVLS ops need the TMA engine (themis_comm_set_engine(comm, 1))");
+  if ((!c->engine || host_seq) && pl->bind->ll)
+    return fail(THEMIS_ERR_INVALID_ARG, "LL plans need the TMA engine and device buffers (rebind with themis_comm_set_ll(comm, 0, 0))");
   const void* fn = kernel_for(dtype, c->engine);
   if (c->trace_on) {  // op start = earliest working CTA (atomicMin over an all-ones start)
     cudaError_t m = cudaMemsetAsync(c->trace, 0xFF, 2 * kMaxOps * sizeof(uint64_t), static_cast<cudaStream_t>(stream));

@@ -336,6 +336,29 @@ __device__ __forceinline__ void mc_st(void* mc, const uint4& v) {  // 16 bytes, 
                :: "l"(mc), "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
                   "f"(__uint_as_float(v.w)) : "memory");
 }
+// LL packets (R31): 16 payload bytes as four 8-byte {payload u32, tag u32}
+// packets, each a single-copy-atomic 64-bit store (two 16-byte vector stores)
+__device__ __forceinline__ void st_ll(void* dst, const uint4& v, uint32_t tag) {
+  const unsigned long long a = (unsigned long long)v.x | ((unsigned long long)tag << 32);
+  const unsigned long long b = (unsigned long long)v.y | ((unsigned long long)tag << 32);
+  const unsigned long long c = (unsigned long long)v.z | ((unsigned long long)tag << 32);
+  const unsigned long long d = (unsigned long long)v.w | ((unsigned long long)tag << 32);
+  char* p = static_cast<char*>(dst);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p + 16), "l"(c), "l"(d) : "memory");
+}
+// one poll of four packets: true (and the payload) if all carry `tag`
+__device__ __forceinline__ bool ld_ll_try(const void* src, uint32_t tag, uint4& v) {
+  const char* p = static_cast<const char*>(src);
+  unsigned long long a, b, c, d;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(d) : "l"(p + 16) : "memory");
+  if ((uint32_t)(a >> 32) != tag || (uint32_t)(b >> 32) != tag || (uint32_t)(c >> 32) != tag ||
+      (uint32_t)(d >> 32) != tag)
+    return false;
+  v = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)c, (uint32_t)d);
+  return true;
+}
 __device__ __forceinline__ void mbar_arrive_token(uint64_t* bar) {  // a zero-byte "go" for a ring slot
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -22,7 +22,9 @@ constexpr int kMaxCtas = 160;  // CTAs per dimension group (ring step flags)
 enum UnitMode { U_DIRECT_RS = 0, U_DIRECT_AG = 1, U_RING_RS = 2, U_RING_AG = 3, U_DIRECT_AG_T = 4,
                 U_NVLS = 5,   // fused NVLS All-Reduce of the own piece on a switch dim (RS op of an RS+AG pair)
                 U_NONE = 6,   // its AG partner: no data (the NVLS broadcast delivered it), dependencies only
-                U_PUSH_AG = 7 };  // direct AG by writes: the own held part -> every dim peer (TMA bulk stores, R30)
+                U_PUSH_AG = 7,    // direct AG by writes: the own held part -> every dim peer (TMA bulk stores, R30)
+                U_LL_RS = 8,      // small-collective RS: 8-byte {payload, epoch} packets pushed into the peers' inboxes (R31)
+                U_LL_AG = 9 };    // small-collective AG, same packets
 
 // Per-op descriptor uploaded at bind (a5).
 struct OpDesc {
@@ -34,6 +36,8 @@ struct OpDesc {
   int32_t push;                      // 1: direct AG executed as pushes (U_PUSH_AG, R30)
   int32_t prev_push;                 // the chunk's previous stage was a push: wait for its k x k' plane (R30)
   int32_t prev_dim;                  // dim of stage - 1 (-1: first stage)
+  int32_t ll;                        // 1: LL packets (R31): no peer flags, the data carries the epoch
+  uint64_t ll_off;                   // byte offset of this op's region in every rank's LL inbox
   int32_t seq;                       // index of the op in its dim's enforced list
   int32_t width, offset;             // the op runs on CTAs [offset, offset+width) mod c_k of its group
   float pace_scale;                  // pacing: width / c_k for a lone narrow op (it gets the whole dim rate), else 1
@@ -70,6 +74,8 @@ struct KParams {
   int32_t lookahead;        // runtime intra-dim order: ops of the enforced list a producer may pick from (<= 1: static)
   uint32_t dyn_mask;        // dims whose ops may be reordered at run time (no ring steps)
   int32_t push_ok;          // push AG allowed in this launch (off while host-buffer streaming)
+  uint64_t ll_rel;          // LL inboxes: heap + ll_rel + (q % V) * ll_stride (R31)
+  uint64_t ll_stride;
   int32_t stages;           // TMA ring depth in use: bytes in flight per CTA = stages x stage_bytes
   int32_t stage_bytes;      // bytes per ring stage (stages x stage_bytes <= kStages x kStageBytes)
   int32_t ag_rr;            // direct AG: 1 = one peer per ring stage (round robin), 0 = all peers per stage
@@ -111,6 +117,9 @@ __device__ __forceinline__ uint32_t* h2d_slot(const KParams& p, int g, int c) {
 }
 __device__ __forceinline__ char* data_of(const KParams& p, int q) {
   return p.heap[q / p.V] + p.data_rel + (uint64_t)(q % p.V) * p.vrank_stride;
+}
+__device__ __forceinline__ char* inbox_of(const KParams& p, int q) {
+  return p.heap[q / p.V] + p.ll_rel + (uint64_t)(q % p.V) * p.ll_stride;
 }
 // 32-bit arithmetic: a comm hosts <= 64 logical ranks (64-bit division is emulated)
 __device__ __forceinline__ int coord(const KParams& p, int q, int k) {
@@ -190,6 +199,7 @@ __device__ __forceinline__ int unit_mode(const OpDesc& d) {
 __device__ __forceinline__ bool is_push(const KParams& p, const OpDesc& d) { return d.push && p.push_ok; }
 __device__ __forceinline__ int unit_mode_tma(const KParams& p, const OpDesc& d) {
   if (d.nvls) return d.nvls == 1 ? U_NVLS : U_NONE;
+  if (d.ll) return d.phase == 0 ? U_LL_RS : U_LL_AG;
   if (is_push(p, d)) return U_PUSH_AG;
   const int m = unit_mode(d);
   return m == U_DIRECT_AG ? U_DIRECT_AG_T : m;
@@ -228,7 +238,7 @@ __device__ __forceinline__ Item decode_item(const KParams& p, const OpDesc& d, i
     f = it - vq * nblk;
     r.j = -1;
     const int ck = coord(p, r.q, k);
-    digit = (mode == U_DIRECT_RS || mode == U_NVLS || mode == U_PUSH_AG) ? ck
+    digit = (mode == U_DIRECT_RS || mode == U_NVLS || mode == U_PUSH_AG || mode == U_LL_RS || mode == U_LL_AG) ? ck
           : mode == U_DIRECT_AG_T ? 0  // base: part j is at off + j * part_stride
           : mode == U_RING_RS     ? (ck + pk - 2 - step) % pk
                                   : ((ck - 1 - step) % pk + pk) % pk;
@@ -363,7 +373,8 @@ __device__ __forceinline__ bool empty_wait(const KParams& p, uint64_t* bar, uint
 __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
                                              char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr,
                                              double& due) {
-  if (mode == U_NVLS || mode == U_NONE) {  // no TMA: a zero-byte token tells the consumers the deps hold
+  if (mode == U_NVLS || mode == U_NONE || mode == U_LL_RS || mode == U_LL_AG) {
+    // no TMA: a zero-byte token tells the consumers the deps hold
     const int s = ctr % p.stages;
     if (!empty_wait(p, &empty[s], ((ctr / p.stages) & 1) ^ 1)) return false;
     dev::mbar_arrive_token(&full[s]);
@@ -438,6 +449,25 @@ __device__ __forceinline__ bool produce_unit(const KParams& p, const OpDesc& d, 
   return ok;
 }
 
+// R31: poll one LL packet group until it carries this launch's tag; the
+// watchdog (timeout -> abort + THEMIS_ERR_TIMEOUT) as in wait_geq.
+__device__ bool ll_wait(const KParams& p, const char* src, uint32_t tag, uint4& v) {
+  if (dev::ld_ll_try(src, tag, v)) return true;
+  const uint64_t t0 = dev::globaltimer();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 256; ++i)
+      if (dev::ld_ll_try(src, tag, v)) return true;
+    if (*(volatile uint32_t*)p.abort_flag) return false;
+    if (dev::globaltimer() - t0 > p.timeout_ns) {
+      atomicExch(p.abort_flag, 1u);
+      *(volatile uint32_t*)p.herr = (uint32_t)THEMIS_ERR_TIMEOUT | (0xFFFFFBu << 8);
+      __threadfence_system();
+      return false;
+    }
+  }
+}
+
 // Hand a ring slot back to the producer after this warp's reads of it: a
 // release arrive (the reads happen-before the producer's acquire and its next
 // TMA write into the slot; measured: no cost over a relaxed arrive).
@@ -453,6 +483,73 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
   const uint32_t tile = unit_tile(p, nsrc), tile16 = tile / 16;
   const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
   bool ok = true;
+  if (mode == U_LL_RS || mode == U_LL_AG) {
+    // R31: no flags between ranks -- every 8-byte packet {4 payload bytes,
+    // epoch} is one single-copy-atomic store into the receiver's inbox and the
+    // receiver polls the packets themselves.  Per 16 payload bytes: send the
+    // peers what they need from this rank (posted writes, never blocking), then
+    // poll what this rank needs from them; every rank's CTA g covers the same
+    // byte ranges (same plan / windows), so the exchange is pairwise.
+    if (!unit_has_work(p, d, mode, gi, gn)) return true;
+    const int s = ctr % p.stages;
+    if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
+    const int k = d.dim, pk = p.size[k];
+    const uint32_t tag = cur_epoch();
+    const uint64_t ps = part_stride(p, k), Lb = p.slice_elems * p.elem_size, nblk = (uint64_t)d.nblk;
+    for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+      if (!ok) return;
+      const Item m = decode_item(p, d, mode, step, it);
+      const int ck = coord(p, m.q, k);
+      const uint64_t f = it % nblk;  // the item's index among its rank's nblk slices
+      for (uint64_t w = a / 16 + ct; w < e / 16; w += kCons) {
+        const uint64_t pos = w * 16;
+        // send: RS -> peer j gets my copy of ITS part; AG -> every peer gets my part
+        for (int j = 0; j < pk; ++j) {
+          if (j == ck) continue;
+          const int qj = m.g0 + j * (int)p.stride[k];
+          const uint64_t src_off = mode == U_LL_RS ? m.off + (int64_t)(j - ck) * (int64_t)ps : m.off;
+          const uint4 v = dev::ld_cg(reinterpret_cast<const uint4*>(data_of(p, m.q) + src_off + pos));
+          const int slot = ck < j ? ck : ck - 1;  // my slot among j's peers
+          char* dst = inbox_of(p, qj) + d.ll_off + (((uint64_t)slot * nblk + f) * Lb + pos) * 2;
+          dev::st_ll(dst, v, tag);
+        }
+        // receive
+        if (mode == U_LL_RS) {
+          float acc[Tag::kAcc];
+          for (int j = 0; j < pk; ++j) {  // coordinate order (R18)
+            uint4 v;
+            if (j == ck) {
+              v = dev::ld_cg(reinterpret_cast<const uint4*>(data_of(p, m.q) + m.off + pos));
+            } else {
+              const int slot = j < ck ? j : j - 1;
+              if (!ll_wait(p, inbox_of(p, m.q) + d.ll_off + (((uint64_t)slot * nblk + f) * Lb + pos) * 2, tag, v)) {
+                ok = false;
+                return;
+              }
+            }
+            if (j == 0) Tag::load(acc, v);
+            else Tag::add(acc, v);
+          }
+          dev::st_v4(reinterpret_cast<uint4*>(data_of(p, m.q) + m.off + pos), Tag::store(acc));
+        } else {
+          for (int j = 0; j < pk; ++j) {
+            if (j == ck) continue;
+            const int slot = j < ck ? j : j - 1;
+            uint4 v;
+            if (!ll_wait(p, inbox_of(p, m.q) + d.ll_off + (((uint64_t)slot * nblk + f) * Lb + pos) * 2, tag, v)) {
+              ok = false;
+              return;
+            }
+            dev::st_v4(reinterpret_cast<uint4*>(data_of(p, m.q) + m.off + (int64_t)(j - ck) * (int64_t)ps + pos), v);
+          }
+        }
+      }
+    });
+    __syncwarp();
+    if (lane == 0) slot_release(p, &empty[s]);
+    ++ctr;
+    return ok;
+  }
   if (mode == U_NVLS || mode == U_NONE) {  // consumers reduce through the switch directly (no ring data)
     if (!unit_has_work(p, d, mode, gi, gn)) return true;
     const int s = ctr % p.stages;
@@ -591,9 +688,11 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
 // k' x k plane through q (P_k' x P_k ranks: q's dim-k peers read data that
 // their dim-k' peers wrote into them).
 __device__ __forceinline__ int n_deps(const KParams& p, const OpDesc& d) {
+  if (d.ll) return 1;  // R31: peers' data arrives tagged in the inbox; only the own (c, s-1) is a flag
   return p.size[d.dim] * ((d.prev_push && p.push_ok) ? p.size[d.prev_dim] : 1);
 }
 __device__ __forceinline__ int dep_src(const KParams& p, const OpDesc& d, int q, int t) {
+  if (d.ll) return q;
   const int k = d.dim, pk = p.size[k];
   int src = q + (t % pk - coord(p, q, k)) * (int)p.stride[k];
   if (d.prev_push && p.push_ok) src += (t / pk - coord(p, q, d.prev_dim)) * (int)p.stride[d.prev_dim];
@@ -710,10 +809,12 @@ __device__ __forceinline__ void complete_op_warp(const KParams& p, const OpDesc&
     // this op wrote into their dim-k peers)
     const bool push = is_push(p, d);
     const int pk = push ? p.size[d.dim] : 1;
-    const int nst = V * pn * pk;
+    const int npe = d.ll ? 1 : pn * pk;  // R31: an LL op's only flag consumer is its own next stage
+    const int nst = V * npe;
     auto dst_of = [&](int t, int& q) {
-      q = q0 + t / (pn * pk);
-      const int u = t % (pn * pk);
+      q = q0 + t / npe;
+      if (d.ll) return q;
+      const int u = t % npe;
       int dst = q + (u % pn - coord(p, q, kn)) * (int)p.stride[kn];
       if (push) dst += (u / pn - coord(p, q, d.dim)) * (int)p.stride[d.dim];
       return dst;

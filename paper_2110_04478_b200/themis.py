@@ -201,6 +201,12 @@ class Plan:
         self.comm = comm
         return self
 
+    def bound_ll(self) -> bool:
+        """True if this bound plan runs with LL packets (R31)."""
+        n = C.c_int32()
+        check(lib().themis_plan_bound_ll(self.h, C.byref(n)))
+        return bool(n.value)
+
     def bound_nvls(self) -> int:
         """RS+AG pairs of this bound plan that run in the switch (R29)."""
         n = C.c_int32()
@@ -244,9 +250,12 @@ class Comm:
     per GPU; heaps are exchanged as CUDA IPC handles over the process group.
     """
 
-    def __init__(self, topo: Topology, data_bytes: int, group=None, device=None, nvls: bool = False):
+    def __init__(self, topo: Topology, data_bytes: int, group=None, device=None, nvls: bool = False,
+                 ll_bytes: int = 0):
         """nvls=True (W > 1): the heap is torch symmetric memory with an NVSwitch
-        multicast mapping, so switch dims can reduce in the switch (R27)."""
+        multicast mapping, so switch dims can reduce in the switch (R27).
+        ll_bytes > 0: reserve an LL inbox of that many bytes per local rank
+        after the data regions (R31; enable with set_ll)."""
         import torch
         self.topo = topo
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -262,6 +271,8 @@ class Comm:
         self.P = topo.P
         self.V = topo.P // self.W
         self.sig_bytes, self.vrank_stride, self.heap_bytes = heap_layout(self.P, self.W, data_bytes)
+        self.ll_stride = (int(ll_bytes) + (1 << 16) - 1) >> 16 << 16
+        self.heap_bytes += self.V * self.ll_stride
         self.imported = []
         self._symm = None
         self.mc_heap = 0
@@ -338,6 +349,13 @@ class Comm:
     def set_window_rotation(self, rotate: bool) -> None:
         """Op windows: consecutive windows (True) or every narrow op from CTA 0."""
         check(lib().themis_comm_set_window_rotation(self.h, int(rotate)))
+
+    def set_ll(self, max_bytes: int, inbox_bytes: Optional[int] = None) -> None:
+        """LL packets for collectives of at most max_bytes per rank (R31);
+        inbox_bytes defaults to the whole inbox reserved at construction.
+        Takes effect at the next Plan.bind; max_bytes = 0 turns it off."""
+        inbox = self.ll_stride if inbox_bytes is None else int(inbox_bytes)
+        check(lib().themis_comm_set_ll(self.h, inbox if max_bytes else 0, int(max_bytes)))
 
     def set_push(self, on: bool) -> None:
         """Direct AG ops by writes (TMA bulk stores into the peers, R30);

@@ -21,18 +21,23 @@ COLL = {S.AR: th.ALLREDUCE, "RS": th.REDUCE_SCATTER, "AG": th.ALL_GATHER}
 KIND_O = {th.RING: T.RING, th.DIRECT: T.DIRECT, th.SWITCH: T.SWITCH}
 
 
-def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None, lookahead=1, push=False):
+def case(group, W, g, sizes, bw, dtype, C, slice_elems, coll, policy, engine, kinds=None, lookahead=1, push=False,
+         ll=False):
     topo = th.Topology(sizes, bw, kinds)
     P = topo.P
     V = P // W
     N = P * C * slice_elems
     esz = ELEM_SIZE[dtype]
-    comm = th.Comm(topo, N * esz, group=group)
+    comm = th.Comm(topo, N * esz, group=group, ll_bytes=4 * N * esz if ll else 0)
+    if ll:
+        comm.set_ll(N * esz)
     comm.set_engine(engine)
     comm.set_timeout(20.0)
     comm.set_lookahead(lookahead)
     comm.set_push(push)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy).bind(comm)
+    if ll and not plan.bound_ll():
+        return [-1]
     xs = host_inputs(P, N, dtype, dist="wide")
     for v in range(V):
         r = g * V + v
@@ -336,6 +341,10 @@ def main():
                       vec * rng.randint(1, 300), rng.choice([S.AR, S.AR, "RS", "AG"]),
                       rng.choice([th.THEMIS, th.BASELINE]), "tma", kinds,
                       rng.choice([1, 4, 16]), rng.random() < 0.5))
+    for sizes, dtype in (((2, 2, 2), "i32"), ((2, 2, 2), "f32"), ((4, 2), "bf16"), ((2, 4), "i32"), ((8,), "f32")):
+        for coll in (S.AR, "RS", "AG"):                                          # R31 LL small collectives
+            cases.append((sizes, tuple([1] * len(sizes)), dtype, 8, (16 // ELEM_SIZE[dtype]) * 97, coll, th.THEMIS,
+                          "tma", None, 1, False, True))
     fails = []
     for c in cases:
         if int(np.prod(c[0])) % W:

@@ -42,12 +42,14 @@ def oracle_sched(sizes, bw, coll, nbytes, C, policy, intra=E.SCF, kinds=None):
 
 def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engine="tma", ctas=None,
              intra=th.SCF, repeat=1, kinds=None, dist="recipe", min_cta_bytes=0, concurrency=1, rotate=1,
-             lookahead=1, push=False):
+             lookahead=1, push=False, ll=False):
     topo = th.Topology(tuple(sizes), tuple(bw), tuple(kinds) if kinds else None)
     P = topo.P
     N = P * C * slice_elems
     esz = ELEM_SIZE[dtype]
-    comm = th.Comm(topo, N * esz)
+    comm = th.Comm(topo, N * esz, ll_bytes=(4 * N * esz if ll else 0))
+    if ll:
+        comm.set_ll(N * esz)
     comm.set_engine(engine)
     comm.set_timeout(10.0)
     comm.set_min_cta_bytes(min_cta_bytes)
@@ -55,6 +57,8 @@ def run_case(sizes, bw, dtype, C, slice_elems, coll=S.AR, policy=th.THEMIS, engi
     comm.set_lookahead(lookahead)
     comm.set_push(push)
     plan = th.Plan(topo, COLL[coll], N * esz, C, policy, intra, concurrency=concurrency).bind(comm, ctas)
+    if ll and not any(k == th.RING and s_ >= 3 for k, s_ in zip(kinds or (), sizes)):
+        assert plan.bound_ll()
     try:
         xs = host_inputs(P, N, dtype, dist=dist)
         for it in range(repeat):
@@ -330,7 +334,8 @@ def test_watchdog_on_missing_peer():
     lib().themis_heap_free(h1)
 
 
-def test_watchdog_mid_collective():
+@pytest.mark.parametrize("ll", [False, True])
+def test_watchdog_mid_collective(ll):
     """a peer that passes the entry barrier but never publishes a
     stage's ready flags must time out *after* other dimension groups started
     streaming (producers blocked on ring slots give up on the abort flag) and
@@ -343,8 +348,10 @@ def test_watchdog_mid_collective():
     from paper_2110_04478_b200._lib import MAX_GPUS, check, lib
     topo = th.Topology((2, 2), (1, 1))
     P, C_ = 4, 16
-    N = P * C_ * (1 << 18)                                  # 64 MiB fp32 per rank: dim1 streams for ms
+    N = P * C_ * (1 << (14 if ll else 18))                  # 64 MiB fp32 per rank: dim1 streams for ms
     sig, stride, hb = th.heap_layout(P, 2, N * 4)
+    inbox = (16 << 20) if ll else 0                        # R31 inboxes after the data regions
+    hb += 2 * inbox
     h0, h1 = C.c_void_p(), C.c_void_p()
     check(lib().themis_heap_alloc(hb, C.byref(h0)))
     check(lib().themis_heap_alloc(hb, C.byref(h1)))
@@ -354,7 +361,13 @@ def test_watchdog_mid_collective():
     check(lib().themis_comm_create(0, 2, C.byref(tc), heaps, hb, stride, C.byref(comm)))
     check(lib().themis_comm_set_timeout(comm, int(0.5e9)))
     plan = th.Plan(topo, th.ALLREDUCE, N * 4, C_, th.THEMIS)
+    if ll:   # R31: the silent peer never sends its LL packets
+        check(lib().themis_comm_set_ll(comm, inbox, N * 4))
     check(lib().themis_plan_bind(plan.h, comm, None))
+    if ll:
+        n = C.c_int32()
+        check(lib().themis_plan_bound_ll(plan.h, C.byref(n)))
+        assert n.value == 1
     hsh = C.c_uint64()
     check(lib().themis_plan_launch_hash(plan.h, N, 0, C.byref(hsh)))
     # signal pad of local rank v: [entry u32 P][exit u32 P][ready u32 P x kMaxOps][ring u64 P x 8 x 160][hash u64 P]
@@ -552,6 +565,55 @@ def test_push_all_gather(sizes, kinds, la):
     want = O.run_schedule(xs, sched, "i32")
     for r in range(P):
         assert np.array_equal(outs[r], want[r]), f"AG rank {r}"
+
+
+@pytest.mark.parametrize("sizes,kinds", [((2, 2, 2), None), ((4, 2), None), ((2, 4), None), ((8,), None),
+                                         ((3, 2), None), ((2, 2, 2, 2), None), ((4, 4), (th.SWITCH, th.DIRECT))])
+def test_ll_small_collectives(sizes, kinds):
+    """R31: LL packets (payload + epoch in every 8-byte store, receivers poll
+    the data) -- AR bit-exact against the oracle (same coordinate-order sums),
+    int32 exact, repeated calls (epoch tags), op windows; RS / AG halves."""
+    kw = dict(kinds=kinds, ll=True, repeat=3)
+    check_ar(sizes, (1,) * len(sizes), "i32", 8, 4 * 100, **kw)
+    check_ar(sizes, (4,) + (1,) * (len(sizes) - 1), "f32", 4, 4 * 101, dist="wide", **kw)
+    check_ar(sizes, (1,) * len(sizes), "bf16", 8, 8 * 33, dist="wide", min_cta_bytes=2048, ctas=[3] * len(sizes), **kw)
+    P = int(np.prod(sizes))
+    for coll in ("RS", "AG"):
+        xs, outs = run_case(sizes, (2,) * len(sizes), "i32", 4, 4 * 57, coll, th.THEMIS, kinds=kinds, ll=True)
+        N = xs[0].shape[0]
+        sched = oracle_sched(sizes, (2,) * len(sizes), coll, N * 4, 4, th.THEMIS, kinds=kinds)
+        want = O.run_schedule(xs, sched, "i32")
+        blk = N // P
+        for r in range(P):
+            got = outs[r][r * blk:(r + 1) * blk] if coll == "RS" else outs[r]
+            exp = want[r][r * blk:(r + 1) * blk] if coll == "RS" else want[r]
+            assert np.array_equal(got, exp), f"{coll} rank {r}"
+
+
+def test_ll_falls_back_when_the_inbox_is_too_small():
+    """A plan whose LL regions do not fit the inbox binds without LL (pull
+    path) and stays exact; ring dims never run LL."""
+    topo = th.Topology((2, 2), (1, 1))
+    N = 4 * 8 * 256
+    comm = th.Comm(topo, N * 4, ll_bytes=1 << 16)
+    try:
+        comm.set_ll(N * 4, 4096)                      # far too small for this plan's regions
+        plan = th.Plan(topo, th.ALLREDUCE, N * 4, 8).bind(comm)
+        assert not plan.bound_ll()
+        plan.close()
+        comm.set_ll(N * 4)
+        plan = th.Plan(topo, th.ALLREDUCE, N * 4, 8).bind(comm)
+        assert plan.bound_ll()
+        plan.close()
+        rt = th.Topology((3, 2), (1, 1), (th.RING, th.DIRECT))
+        comm2 = th.Comm(rt, 6 * 8 * 256 * 4, ll_bytes=1 << 20)
+        comm2.set_ll(1 << 20)
+        plan = th.Plan(rt, th.ALLREDUCE, 6 * 8 * 256 * 4, 8).bind(comm2)
+        assert not plan.bound_ll()
+        plan.close()
+        comm2.close()
+    finally:
+        comm.close()
 
 
 def test_max_ranks_and_many_chunks():
