@@ -486,37 +486,48 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
   if (mode == U_LL_RS || mode == U_LL_AG) {
     // R31: no flags between ranks -- every 8-byte packet {4 payload bytes,
     // epoch} is one single-copy-atomic store into the receiver's inbox and the
-    // receiver polls the packets themselves.  Per 16 payload bytes: send the
-    // peers what they need from this rank (posted writes, never blocking), then
-    // poll what this rank needs from them; every rank's CTA g covers the same
-    // byte ranges (same plan / windows), so the exchange is pairwise.
+    // receiver polls the packets themselves.  Two passes over this CTA's
+    // span: send the peers what they need from this rank, then poll what this
+    // rank needs from them.
     if (!unit_has_work(p, d, mode, gi, gn)) return true;
     const int s = ctr % p.stages;
     if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
     const int k = d.dim, pk = p.size[k];
     const uint32_t tag = cur_epoch();
     const uint64_t ps = part_stride(p, k), Lb = p.slice_elems * p.elem_size, nblk = (uint64_t)d.nblk;
+    // pass 1: send everything in this CTA's span (posted writes, never block)
     for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
-      if (!ok) return;
       const Item m = decode_item(p, d, mode, step, it);
       const int ck = coord(p, m.q, k);
       const uint64_t f = it % nblk;  // the item's index among its rank's nblk slices
       for (uint64_t w = a / 16 + ct; w < e / 16; w += kCons) {
         const uint64_t pos = w * 16;
-        // send: RS -> peer j gets my copy of ITS part; AG -> every peer gets my part
+        // RS: peer j gets my copy of ITS part; AG: every peer gets my part
         for (int j = 0; j < pk; ++j) {
           if (j == ck) continue;
           const int qj = m.g0 + j * (int)p.stride[k];
           const uint64_t src_off = mode == U_LL_RS ? m.off + (int64_t)(j - ck) * (int64_t)ps : m.off;
           const uint4 v = dev::ld_cg(reinterpret_cast<const uint4*>(data_of(p, m.q) + src_off + pos));
           const int slot = ck < j ? ck : ck - 1;  // my slot among j's peers
-          char* dst = inbox_of(p, qj) + d.ll_off + (((uint64_t)slot * nblk + f) * Lb + pos) * 2;
-          dev::st_ll(dst, v, tag);
+          dev::st_ll(inbox_of(p, qj) + d.ll_off + (((uint64_t)slot * nblk + f) * Lb + pos) * 2, v, tag);
         }
-        // receive
+      }
+    });
+    // every consumer thread of this CTA has sent before any waits: a CTA that
+    // hosts several local ranks never waits on its own unsent packets, and
+    // the receive pass mostly finds packets already landed
+    dev::named_bar_sync(1, kCons);
+    // pass 2: receive, reduce in coordinate order (R18) / copy
+    for_each_span(p, d, mode, gi, gn, [&](uint64_t it, uint64_t a, uint64_t e) {
+      if (!ok) return;
+      const Item m = decode_item(p, d, mode, step, it);
+      const int ck = coord(p, m.q, k);
+      const uint64_t f = it % nblk;
+      for (uint64_t w = a / 16 + ct; w < e / 16; w += kCons) {
+        const uint64_t pos = w * 16;
         if (mode == U_LL_RS) {
           float acc[Tag::kAcc];
-          for (int j = 0; j < pk; ++j) {  // coordinate order (R18)
+          for (int j = 0; j < pk; ++j) {
             uint4 v;
             if (j == ck) {
               v = dev::ld_cg(reinterpret_cast<const uint4*>(data_of(p, m.q) + m.off + pos));
