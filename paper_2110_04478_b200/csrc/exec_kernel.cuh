@@ -491,7 +491,11 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
     // rank needs from them.
     if (!unit_has_work(p, d, mode, gi, gn)) return true;
     const int s = ctr % p.stages;
-    if (!dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)) return false;
+    // the consumer warps meet at a named barrier below: decide "go / abort"
+    // for all of them at once (a warp that saw the abort flag while another
+    // saw the token must not leave the others waiting at the barrier)
+    if (!dev::named_bar_and(1, kCons, dev::mbar_wait_or(&full[s], (ctr / p.stages) & 1, p.abort_flag)))
+      return false;
     const int k = d.dim, pk = p.size[k];
     const uint32_t tag = cur_epoch();
     const uint64_t ps = part_stride(p, k), Lb = p.slice_elems * p.elem_size, nblk = (uint64_t)d.nblk;

@@ -595,7 +595,7 @@ def test_ll_falls_back_when_the_inbox_is_too_small():
     path) and stays exact; ring dims never run LL."""
     topo = th.Topology((2, 2), (1, 1))
     N = 4 * 8 * 256
-    comm = th.Comm(topo, N * 4, ll_bytes=1 << 16)
+    comm = th.Comm(topo, N * 4, ll_bytes=1 << 20)
     try:
         comm.set_ll(N * 4, 4096)                      # far too small for this plan's regions
         plan = th.Plan(topo, th.ALLREDUCE, N * 4, 8).bind(comm)
