@@ -560,7 +560,9 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
         }
       }
     });
-    __syncwarp();
+    // a thread with nothing left to poll must not run on while others gave up
+    // (the next LL unit's barrier would wait for them): one answer per CTA
+    ok = dev::named_bar_and(1, kCons, ok);
     if (lane == 0) slot_release(p, &empty[s]);
     ++ctr;
     return ok;
@@ -1070,7 +1072,8 @@ __global__ void __launch_bounds__(kThreads, 1) themis_exec_kernel(const __grid_c
         const int nu = d.ring ? p.size[d.dim] - 1 : 1;
         int li, wn;
         op_member(d, gi, gn, li, wn);
-        if (!consume_unit<Tag>(p, d, mode, u, li, wn, smem, full, empty, ctr)) break;
+        // warp-uniform: a lane whose spans ended before an abort must stop with the others
+        if (!__all_sync(0xFFFFFFFFu, consume_unit<Tag>(p, d, mode, u, li, wn, smem, full, empty, ctr))) break;
         __syncwarp();
         bool w = true;
         if (lane == 0) {
