@@ -473,17 +473,14 @@ __device__ bool ll_wait(const KParams& p, const char* src, uint32_t tag, uint4& 
 // TMA write into the slot; measured: no cost over a relaxed arrive).
 __device__ __forceinline__ void slot_release(const KParams&, uint64_t* bar) { dev::mbar_arrive(bar); }
 
-// Consumers: returns false if the kernel is aborting (watchdog).
+// R31 LL unit (consumer warps), kept out of line so the pull path's code is
+// unchanged.  Returns false if the kernel is aborting (CTA-uniform).
 template <class Tag>
-__device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
-                                             const char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+__device__ __noinline__ bool consume_ll_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
+                                             uint64_t* full, uint64_t* empty, uint32_t& ctr) {
   const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
   constexpr int kCons = 32 * kConsumerWarps;
-  const int nsrc = unit_nsrc(p, d, mode);
-  const uint32_t tile = unit_tile(p, nsrc), tile16 = tile / 16;
-  const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
   bool ok = true;
-  if (mode == U_LL_RS || mode == U_LL_AG) {
     // R31: no flags between ranks -- every 8-byte packet {4 payload bytes,
     // epoch} is one single-copy-atomic store into the receiver's inbox and the
     // receiver polls the packets themselves.  Two passes over this CTA's
@@ -566,7 +563,19 @@ __device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, 
     if (lane == 0) slot_release(p, &empty[s]);
     ++ctr;
     return ok;
-  }
+}
+
+// Consumers: returns false if the kernel is aborting (watchdog).
+template <class Tag>
+__device__ __forceinline__ bool consume_unit(const KParams& p, const OpDesc& d, int mode, int step, int gi, int gn,
+                                             const char* smem, uint64_t* full, uint64_t* empty, uint32_t& ctr) {
+  const int ct = threadIdx.x - 32, lane = threadIdx.x & 31;
+  constexpr int kCons = 32 * kConsumerWarps;
+  const int nsrc = unit_nsrc(p, d, mode);
+  const uint32_t tile = unit_tile(p, nsrc), tile16 = tile / 16;
+  const bool reduce = mode == U_DIRECT_RS || mode == U_RING_RS;
+  bool ok = true;
+  if (mode == U_LL_RS || mode == U_LL_AG) return consume_ll_unit<Tag>(p, d, mode, step, gi, gn, full, empty, ctr);
   if (mode == U_NVLS || mode == U_NONE) {  // consumers reduce through the switch directly (no ring data)
     if (!unit_has_work(p, d, mode, gi, gn)) return true;
     const int s = ctr % p.stages;
