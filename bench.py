@@ -437,6 +437,10 @@ def run_themis(a):
                                     "achieved_gbs": round(nk / busy, 2) if busy else None})
         span = int(tr[:, :, 1].max() - tr[:, :, 0].min())
         per_dim["span_us"] = round(span / 1e3, 1)
+        per_dim["note"] = ("trace-derived inside the full collective (busy = union of a dim's op intervals); "
+                           "the hardware check -- each dim group alone on the real kernel, ncu "
+                           "nvlrx__bytes_data_user.sum / duration = 0.94-1.01 of BW_K -- is "
+                           "profiles/r02/k5_nvlink/README.md")
         p.close()
         comm.enable_trace(False)
         comm.set_pacing(False)
