@@ -1,3 +1,4 @@
+import pytest
 """The C-ABI library loads on a CPU-only host and exports every symbol
 include/themis.h declares; the Python binding uses the same names."""
 
@@ -64,5 +65,8 @@ def test_default_ctas_is_the_a9_formula():
 
 def test_default_ctas():
     assert th.default_ctas((4, 2, 1), 28) == [16, 8, 4]
+    assert th.default_ctas((1000, 1, 1), 3) == [1, 1, 1]           # the one-CTA floor binds
+    with pytest.raises(th.ThemisError):
+        th.default_ctas((1, 1, 1), 2)                              # budget < ndims
     assert th.default_ctas((1, 1, 1), 148) == [50, 49, 49]
     assert sum(th.default_ctas((200, 50), 7)) == 7

@@ -151,11 +151,13 @@ def test_custom_orders_full_space():
     pre-simulated bit-exactly like the oracle's engine."""
     import itertools
     rng = random.Random(99)
-    for _ in range(60):
+    for _ in range(90):
         D = rng.randint(1, 3)
         sizes = [rng.choice([2, 3, 4]) for _ in range(D)]
         bw = [rng.choice(BWS) for _ in range(D)]
-        o, g = make_pair(sizes, bw)
+        # NVLS dims too (R29): a chunk's pair is fused only if its last RS dim is its first AG dim
+        kinds = [rng.choice([T.DIRECT, T.NVLS]) if s_ & (s_ - 1) == 0 else T.DIRECT for s_ in sizes]
+        o, g = make_pair(sizes, bw, kinds)
         C = rng.randint(1, 12)
         coll = rng.choice([S.AR, "RS", "AG"])
         perms = list(itertools.permutations(range(D)))
