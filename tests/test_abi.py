@@ -1,6 +1,7 @@
-import pytest
 """The C-ABI library loads on a CPU-only host and exports every symbol
 include/themis.h declares; the Python binding uses the same names."""
+
+import pytest
 
 import os
 import re
